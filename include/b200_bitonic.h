@@ -1,0 +1,143 @@
+/*
+ * b200_bitonic.h -- C ABI of the B200-native bitonic sort (sm_100a).
+ *
+ * Drop-in boundary for the hot path of arxiv/paper_1506_01446's artifact:
+ * the reference's C++ entry points (namespace bitonic, /root/reference/proj)
+ * sort a power-of-two array of 32-bit keys in place on the CPU.  These C
+ * functions replace them with CUDA kernels; C++ callers use the thin shim
+ * include/bitonic/gpu_sort.hpp, which maps the status codes below back onto
+ * the reference's exception types.  No torch types cross this boundary.
+ *
+ * Status codes (returned by every function):
+ *   0 B200_OK
+ *   1 B200_INVALID_SIZE   -> bitonic::invalid_size_error  (error.hpp:11-15):
+ *                            n < 2, n not a power of two, n too large
+ *   2 B200_CONFIG         -> bitonic::config_error        (error.hpp:19-23):
+ *                            bad argument (null pointer, misaligned pointer,
+ *                            ngpu not in {1,2,4,8}, bad batch, ...)
+ *   3 B200_CUDA_ERROR     CUDA runtime failure (message in last_error)
+ *   4 B200_NCCL_ERROR     reserved for the NCCL exchange path
+ * There is no CPU fallback: a missing/unsupported GPU is B200_CUDA_ERROR.
+ *
+ * Device-pointer entry points are stream-ordered and asynchronous: they
+ * enqueue kernels on `stream` and return; they allocate nothing (bitonic is
+ * in place).  They are reentrant per stream.
+ */
+#ifndef B200_BITONIC_H
+#define B200_BITONIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Compatible with the CUDA runtime's own typedef. */
+struct CUstream_st;
+typedef struct CUstream_st* b200_stream_t;
+
+enum {
+  B200_OK = 0,
+  B200_INVALID_SIZE = 1,
+  B200_CONFIG = 2,
+  B200_CUDA_ERROR = 3,
+  B200_NCCL_ERROR = 4
+};
+
+/* In-place sort of n uint32 keys at device pointer d_keys.
+ * Replaces bitonic::sequential_bitonic_sort(std::span<int32_t>)
+ * (proj/include/bitonic/engine.hpp:102-104, proj/src/engine.cpp:248-266)
+ * and bitonic::execute(build_plan(...), keys, workers) (engine.hpp:77-92),
+ * with the uint32 key order BASELINE.json's metric uses and a new
+ * `descending` flag (0 = ascending, the reference's only order; 1 =
+ * std::greater order).  n must be a power of two >= 2 (same contract as
+ * engine.cpp:250-253); d_keys must be 16-byte aligned when n >= 4. */
+int b200_bitonic_sort_u32(uint32_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream);
+
+/* Same with the reference's own key type and order (signed int32,
+ * engine.hpp:13-15).  Bit-identical to sequential_bitonic_sort's output. */
+int b200_bitonic_sort_i32(int32_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream);
+
+/* `batch` independent contiguous arrays of n_per_array keys each, every one
+ * sorted on its own (BASELINE config "4096 arrays of 2^12").  n_per_array
+ * must be a power of two >= 2; batch >= 1. */
+int b200_bitonic_sort_u32_batched(uint32_t* d_keys, uint64_t n_per_array,
+                                  uint64_t batch, int descending,
+                                  b200_stream_t stream);
+int b200_bitonic_sort_i32_batched(int32_t* d_keys, uint64_t n_per_array,
+                                  uint64_t batch, int descending,
+                                  b200_stream_t stream);
+
+/* Host-memory convenience entries: H2D copy, sort, D2H copy, synchronous.
+ * Mirror sequential_bitonic_sort(std::span<int32_t>) exactly (in place on
+ * caller-owned host memory).  These allocate device memory per call. */
+int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending);
+int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending);
+
+/* Partitioned sort over ngpu GPUs driven from one host thread.
+ * d_shards[r] is a device pointer on device devices[r] holding the
+ * contiguous slice r (work_slice rule, worker_pool.hpp:22-25) of an array of
+ * n_total keys; each shard holds n_total/ngpu keys.  On return rank r holds
+ * global sorted positions [r*m, (r+1)*m).  ngpu in {1,2,4,8}; devices may
+ * repeat (then the "ranks" share one GPU and exchange through its memory).
+ * Each rank sorts locally, then a rank-level bitonic network of merge-split
+ * steps runs; the merge kernel reads the partner's shard directly through
+ * CUDA peer memory (NVLink).  Synchronous.  Allocates one scratch shard per
+ * rank. */
+int b200_bitonic_sort_u32_multi(uint32_t* const* d_shards, const int* devices,
+                                int ngpu, uint64_t n_total, int descending);
+
+/* One merge-split step (the building block of the partitioned sort, exposed
+ * for multi-process drivers that move shards with NCCL): local and partner
+ * are sorted (ascending in the order given by key_xor: 0 = uint32,
+ * 0x80000000 = int32, ~0 = descending uint32); out receives the m smallest
+ * (keep_high = 0) or m largest (keep_high = 1) keys of their union, sorted
+ * in the same order.  out must not alias either input.  partner may be a
+ * peer-device pointer. */
+int b200_bitonic_merge_split_u32(const uint32_t* local, const uint32_t* partner,
+                                 uint64_t m, int keep_high, uint32_t key_xor,
+                                 uint32_t* out, b200_stream_t stream);
+
+/* ---- plan introspection (host only, no GPU needed) ----------------------
+ * One entry per kernel launch of the sort of `batch` arrays of n keys. */
+typedef struct {
+  int tile_bits;  /* C: keys per CTA = 2^C                                  */
+  int a;          /* low local bits = global bits [0, a)                    */
+  int y;          /* high local bits = global bits [y, y + C - a)           */
+  int tile_sort;  /* 1 = phases 1..C in one pass                           */
+  int segA_hi;    /* tail CE bits segA_hi..0 of phase pA (-1 = none)        */
+  int pA;
+  int segB_lo;    /* head CE bits C-1..segB_lo (local) of phase pB (-1 = none) */
+  int pB;
+  uint64_t ctas;  /* grid size                                              */
+  uint64_t compare_exchanges; /* CEs executed by this launch               */
+} b200_pass_info;
+
+/* Fills up to max_passes entries; *n_passes receives the plan length. */
+int b200_bitonic_plan(uint64_t n, uint64_t batch, b200_pass_info* out,
+                      int max_passes, int* n_passes);
+
+/* Counters in the reference's cost model (engine.hpp:55-70, account() in
+ * engine.cpp:147-173): {kernel_launches, global_reads, global_writes,
+ * compare_exchanges}; reads/writes count keys (x4 for bytes). */
+int b200_bitonic_counters(uint64_t n, uint64_t batch, uint64_t out[4]);
+
+/* Tuning knobs (process-wide; for benchmarks and tests).  tile_bits in
+ * [6, 15] caps the CTA tile (default chosen per n); min_run_bits in [2, 10]
+ * is the minimum contiguous run (2^bits keys) every merge pass moves. */
+int b200_bitonic_set_tuning(int tile_bits, int min_run_bits);
+
+/* Thread-local message for the last non-zero status. */
+const char* b200_bitonic_last_error(void);
+
+/* Library version string. */
+const char* b200_bitonic_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B200_BITONIC_H */

@@ -1,0 +1,242 @@
+"""paper_1506_01446_b200 -- B200-native (sm_100a) bitonic sort of 32-bit keys.
+
+Python host mirror of the reference's sort entry points (namespace
+``bitonic`` in /root/reference/proj/include/bitonic), calling the CUDA side
+through the C ABI of include/b200_bitonic.h:
+
+==============================================  ===============================
+reference (C++)                                 here
+==============================================  ===============================
+sequential_bitonic_sort(span<int32_t>)          sequential_bitonic_sort(np.int32 array)
+  engine.hpp:102-104, engine.cpp:248-266          (host array, in place, via GPU)
+execute(build_plan(...), keys, workers)         sort_(tensor, descending)   (device, in place)
+  engine.hpp:77-92
+build_plan / account / Counters                 plan(n), counters(n)
+  engine.hpp:44-84, engine.cpp:86-173
+invalid_size_error (error.hpp:11-15)            InvalidSizeError  (a ValueError)
+config_error       (error.hpp:19-23)            ConfigError       (a ValueError)
+==============================================  ===============================
+
+plus the north_star additions: ``descending``, uint32 keys, batched arrays
+(``sort_batched_``), the partitioned multi-GPU sort (``sort_multi``) and the
+merge-split building block (``merge_split_``).  There is no CPU fallback: the
+native library must be present and a CUDA device must be visible.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native
+
+__all__ = [
+    "InvalidSizeError", "ConfigError", "CudaError",
+    "sort_", "sort_batched_", "sequential_bitonic_sort", "sort_host",
+    "merge_split_", "sort_multi", "plan", "counters", "set_tuning",
+    "PassPlan", "version", "library_path",
+]
+
+
+class InvalidSizeError(ValueError):
+    """Mirror of bitonic::invalid_size_error (std::invalid_argument)."""
+
+
+class ConfigError(ValueError):
+    """Mirror of bitonic::config_error (std::invalid_argument)."""
+
+
+class CudaError(RuntimeError):
+    """A CUDA runtime failure inside the native library."""
+
+
+class NcclError(RuntimeError):
+    """Reserved for the NCCL exchange path."""
+
+
+_ERRORS = {1: InvalidSizeError, 2: ConfigError, 3: CudaError, 4: NcclError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _native.lib().b200_bitonic_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def library_path() -> str:
+    return _native.LIB_PATH
+
+
+def version() -> str:
+    return _native.lib().b200_bitonic_version().decode()
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _key_dtype(t):
+    import torch
+    if t.dtype == torch.int32:
+        return "i32"
+    if t.dtype == torch.uint32:
+        return "u32"
+    raise ConfigError(f"keys must be int32 or uint32, got {t.dtype}")
+
+
+def _check_tensor(t) -> None:
+    if not t.is_cuda:
+        raise ConfigError("sort_ needs a CUDA tensor (use sort_host for host arrays)")
+    if not t.is_contiguous():
+        raise ConfigError("keys must be contiguous")
+
+
+def sort_(t, descending: bool = False, stream=None):
+    """Sort a 1-D CUDA tensor of int32 (signed order, the reference's key type)
+    or uint32 keys in place; asynchronous on ``stream`` (default: current)."""
+    _check_tensor(t)
+    kind = _key_dtype(t)
+    fn = _native.lib().b200_bitonic_sort_i32 if kind == "i32" else _native.lib().b200_bitonic_sort_u32
+    _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
+              ctypes.c_void_p(_stream_ptr(stream))))
+    return t
+
+
+def sort_batched_(t, n_per_array: int, descending: bool = False, stream=None):
+    """Sort ``t.numel() // n_per_array`` contiguous arrays independently."""
+    _check_tensor(t)
+    if n_per_array < 1 or t.numel() % n_per_array:
+        raise ConfigError("numel must be a multiple of n_per_array")
+    kind = _key_dtype(t)
+    fn = (_native.lib().b200_bitonic_sort_i32_batched if kind == "i32"
+          else _native.lib().b200_bitonic_sort_u32_batched)
+    _check(fn(ctypes.c_void_p(t.data_ptr()), n_per_array, t.numel() // n_per_array,
+              int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
+    return t
+
+
+def sort_host(keys: np.ndarray, descending: bool = False) -> np.ndarray:
+    """In-place sort of a host numpy int32/uint32 array (H2D, sort, D2H)."""
+    if not isinstance(keys, np.ndarray) or not keys.flags["C_CONTIGUOUS"]:
+        raise ConfigError("keys must be a C-contiguous numpy array")
+    if keys.dtype == np.int32:
+        fn = _native.lib().b200_bitonic_sort_host_i32
+    elif keys.dtype == np.uint32:
+        fn = _native.lib().b200_bitonic_sort_host_u32
+    else:
+        raise ConfigError(f"keys must be int32 or uint32, got {keys.dtype}")
+    _check(fn(ctypes.c_void_p(keys.ctypes.data), keys.size, int(bool(descending))))
+    return keys
+
+
+def sequential_bitonic_sort(keys: np.ndarray) -> None:
+    """Drop-in for bitonic::sequential_bitonic_sort(std::span<int32_t>)
+    (engine.cpp:248-266): ascending, in place, power-of-two length >= 2,
+    InvalidSizeError otherwise -- but the network runs on the GPU."""
+    if not isinstance(keys, np.ndarray) or keys.dtype != np.int32:
+        raise ConfigError("keys must be a numpy int32 array")
+    sort_host(keys, descending=False)
+
+
+def merge_split_(local, partner, out, keep_high: bool, key_xor: int = 0,
+                 stream=None):
+    """out <- the m smallest (keep_high=False) or largest keys of local U partner
+    (both sorted in the order ``key_xor`` selects: 0 uint32, 0x80000000 int32,
+    0xFFFFFFFF descending uint32)."""
+    for x in (local, partner, out):
+        _check_tensor(x)
+    m = local.numel()
+    if partner.numel() != m or out.numel() != m:
+        raise ConfigError("local, partner and out must have the same length")
+    _check(_native.lib().b200_bitonic_merge_split_u32(
+        ctypes.c_void_p(local.data_ptr()), ctypes.c_void_p(partner.data_ptr()), m,
+        int(bool(keep_high)), ctypes.c_uint32(key_xor & 0xFFFFFFFF),
+        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))))
+    return out
+
+
+def sort_multi(shards: Sequence, descending: bool = False) -> None:
+    """Partitioned sort: shards[r] (uint32, equal sizes, on any devices) are the
+    contiguous slices of one array; afterwards shard r holds sorted positions
+    [r*m, (r+1)*m).  Synchronous; one host thread drives every device."""
+    import torch
+    g = len(shards)
+    ptrs = (ctypes.c_void_p * g)(*[ctypes.c_void_p(s.data_ptr()) for s in shards])
+    devs = (ctypes.c_int * g)(*[s.device.index for s in shards])
+    for s in shards:
+        _check_tensor(s)
+        if s.dtype != torch.uint32:
+            raise ConfigError("sort_multi takes uint32 shards")
+    n_total = sum(s.numel() for s in shards)
+    if len({s.numel() for s in shards}) != 1:
+        raise ConfigError("shards must have equal length")
+    for s in shards:
+        torch.cuda.synchronize(s.device)
+    _check(_native.lib().b200_bitonic_sort_u32_multi(ptrs, devs, g, n_total,
+                                                     int(bool(descending))))
+
+
+@dataclass(frozen=True)
+class PassPlan:
+    tile_bits: int
+    a: int
+    y: int
+    tile_sort: bool
+    segA_hi: int
+    pA: int
+    segB_lo: int
+    pB: int
+    ctas: int
+    compare_exchanges: int
+
+    def step_bits(self) -> List[tuple]:
+        """(phase, global bit) of every network step this pass runs, in order."""
+        out = []
+        C = self.tile_bits
+        if self.tile_sort:
+            for p in range(1, self.pA + 1):
+                for b in range(p - 1, -1, -1):
+                    out.append((p, b))
+            return out
+
+        def glob(l):
+            return l if l < self.a else self.y + (l - self.a)
+
+        if self.segA_hi >= 0:
+            for l in range(self.segA_hi, -1, -1):
+                out.append((self.pA, glob(l)))
+        if self.segB_lo >= 0:
+            for l in range(C - 1, self.segB_lo - 1, -1):
+                out.append((self.pB, glob(l)))
+        return out
+
+
+def plan(n: int, batch: int = 1) -> List[PassPlan]:
+    """The launch plan for ``batch`` arrays of ``n`` keys (host only)."""
+    L = _native.lib()
+    cnt = ctypes.c_int(0)
+    _check(L.b200_bitonic_plan(n, batch, None, 0, ctypes.byref(cnt)))
+    arr = (_native.PassInfo * max(cnt.value, 1))()
+    _check(L.b200_bitonic_plan(n, batch, arr, cnt.value, ctypes.byref(cnt)))
+    return [PassPlan(p.tile_bits, p.a, p.y, bool(p.tile_sort), p.segA_hi, p.pA,
+                     p.segB_lo, p.pB, int(p.ctas), int(p.compare_exchanges))
+            for p in arr[: cnt.value]]
+
+
+def counters(n: int, batch: int = 1) -> dict:
+    """Counters in the reference's model (engine.hpp:55-70): launches, key
+    reads, key writes, compare-exchanges for one sort."""
+    out = (ctypes.c_uint64 * 4)()
+    _check(_native.lib().b200_bitonic_counters(n, batch, out))
+    return {"kernel_launches": int(out[0]), "global_reads": int(out[1]),
+            "global_writes": int(out[2]), "compare_exchanges": int(out[3])}
+
+
+def set_tuning(tile_bits: int = 0, min_run_bits: int = 5) -> None:
+    """tile_bits: 0 = automatic, else 6..15; min_run_bits: 2..10."""
+    _check(_native.lib().b200_bitonic_set_tuning(tile_bits, min_run_bits))

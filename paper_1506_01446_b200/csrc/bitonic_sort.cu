@@ -1,0 +1,483 @@
+// bitonic_sort.cu -- launcher, C ABI, merge-split and the partitioned sort.
+//
+// Host side of the B200-native bitonic sort.  Replaces, behind the C ABI in
+// include/b200_bitonic.h, the reference's execute() (engine.cpp:175-227):
+// where the reference runs each launch of a LaunchPlan on a fork-join worker
+// pool with a full barrier in between (worker_pool.cpp:28-44), this enqueues
+// one sm_100a kernel per planned pass on a CUDA stream; stream order is the
+// barrier.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/b200_bitonic.h"
+#include "bitonic_engine.cuh"
+#include "merge_split.cuh"
+#include "planner.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+std::atomic<int> g_tile_bits{0};  // 0 = automatic
+std::atomic<int> g_min_run_bits{5};
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(B200_CUDA_ERROR,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define B200_CUDA_TRY(expr)                        \
+  do {                                             \
+    cudaError_t _e = (expr);                       \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+b200::PlanOptions plan_options() {
+  b200::PlanOptions o;
+  const int tb = g_tile_bits.load();
+  if (tb > 0) {
+    o.cmax = tb;
+    o.cmin = tb;  // explicit tile size: no automatic shrinking
+  }
+  o.lrun = g_min_run_bits.load();
+  return o;
+}
+
+int log2_exact(uint64_t n) {
+  int k = 0;
+  while ((uint64_t{1} << k) < n) ++k;
+  return k;
+}
+
+bool is_pow2(uint64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+// ---- per-device kernel attributes (max dynamic shared memory) -----------
+template <int C>
+cudaError_t set_attrs() {
+  const int bytes = b200::tile_smem_words(C) * 4;
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(b200::bitonic_pass_kernel<C>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              bytes);
+}
+
+std::mutex g_attr_mu;
+std::vector<int> g_attr_done;
+
+cudaError_t ensure_attrs() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if ((int)g_attr_done.size() <= dev) g_attr_done.resize(dev + 1, 0);
+  if (g_attr_done[dev]) return cudaSuccess;
+  cudaError_t r = cudaSuccess;
+  auto chk = [&](cudaError_t x) { if (r == cudaSuccess && x != cudaSuccess) r = x; };
+  chk(set_attrs<11>());
+  chk(set_attrs<12>());
+  chk(set_attrs<13>());
+  chk(set_attrs<14>());
+  chk(set_attrs<15>());
+  if (r == cudaSuccess) g_attr_done[dev] = 1;
+  return r;
+}
+
+template <int C>
+void launch_c(const b200::PassParams& p, uint64_t ctas, cudaStream_t s) {
+  constexpr int T = b200::tile_threads(C);
+  const size_t smem = (size_t)b200::tile_smem_words(C) * 4;
+  b200::bitonic_pass_kernel<C><<<(unsigned)ctas, T, smem, s>>>(p);
+}
+
+void launch_pass(int C, const b200::PassParams& p, uint64_t ctas,
+                 cudaStream_t s) {
+  switch (C) {
+    case 1: launch_c<1>(p, ctas, s); break;
+    case 2: launch_c<2>(p, ctas, s); break;
+    case 3: launch_c<3>(p, ctas, s); break;
+    case 4: launch_c<4>(p, ctas, s); break;
+    case 5: launch_c<5>(p, ctas, s); break;
+    case 6: launch_c<6>(p, ctas, s); break;
+    case 7: launch_c<7>(p, ctas, s); break;
+    case 8: launch_c<8>(p, ctas, s); break;
+    case 9: launch_c<9>(p, ctas, s); break;
+    case 10: launch_c<10>(p, ctas, s); break;
+    case 11: launch_c<11>(p, ctas, s); break;
+    case 12: launch_c<12>(p, ctas, s); break;
+    case 13: launch_c<13>(p, ctas, s); break;
+    case 14: launch_c<14>(p, ctas, s); break;
+    default: launch_c<15>(p, ctas, s); break;
+  }
+}
+
+// Validates and runs the whole plan.  key_xor: 0x80000000 for int32 keys.
+int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
+              uint32_t key_xor, cudaStream_t stream) {
+  if (n_per < 2 || !is_pow2(n_per)) {
+    return fail(B200_INVALID_SIZE,
+                "length must be a power of two >= 2, got " +
+                    std::to_string(n_per));
+  }
+  if (batch < 1) return fail(B200_CONFIG, "batch must be >= 1");
+  const int k = log2_exact(n_per);
+  if (k > 34 || (batch << k) >> k != batch || (batch << k) > (uint64_t{1} << 35)) {
+    return fail(B200_INVALID_SIZE, "array too large for one device");
+  }
+  if (descending != 0 && descending != 1) {
+    return fail(B200_CONFIG, "descending must be 0 or 1");
+  }
+  if (d_keys == nullptr) return fail(B200_CONFIG, "null key pointer");
+  std::vector<b200::PlanPass> plan;
+  try {
+    plan = b200::make_plan(k, batch, plan_options());
+  } catch (const std::exception& e) {
+    return fail(B200_CONFIG, e.what());
+  }
+  if (plan.front().C >= 2 && (reinterpret_cast<uintptr_t>(d_keys) & 15u) != 0) {
+    return fail(B200_CONFIG, "device pointer must be 16-byte aligned");
+  }
+  B200_CUDA_TRY(ensure_attrs());
+  const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+  for (size_t i = 0; i < plan.size(); ++i) {
+    const b200::PlanPass& q = plan[i];
+    b200::PassParams p{};
+    p.keys = d_keys;
+    p.gmask_in = (i == 0) ? gmask : 0u;
+    p.gmask_out = (i + 1 == plan.size()) ? gmask : 0u;
+    p.a = q.a;
+    p.y = q.y;
+    p.kd = k;
+    p.tile_sort = q.tile_sort;
+    p.p_end = q.p_end;
+    p.segA_hi = q.segA_hi;
+    p.pA = q.pA;
+    p.segB_lo = q.segB_lo;
+    p.pB = q.pB;
+    launch_pass(q.C, p, q.ctas, stream);
+  }
+  B200_CUDA_TRY(cudaGetLastError());
+  return B200_OK;
+}
+
+// ---- merge-split ----------------------------------------------------------
+int merge_split_impl(const uint32_t* local, const uint32_t* partner, uint64_t m,
+                     int keep_high, uint32_t key_xor, uint32_t* out,
+                     uint64_t* scratch_coranks, cudaStream_t s) {
+  const uint64_t tiles = (m + b200::kMergeTile - 1) / b200::kMergeTile;
+  const uint64_t nb = tiles + 1;
+  b200::merge_partition_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
+      local, partner, m, keep_high, key_xor, scratch_coranks, nb);
+  b200::merge_tile_kernel<<<(unsigned)tiles, b200::kMergeThreads, 0, s>>>(
+      local, partner, m, keep_high, key_xor, scratch_coranks, out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "merge-split launch");
+  return B200_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int b200_bitonic_sort_u32(uint32_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream) {
+  return sort_impl(d_keys, n, 1, descending, 0u,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_i32(int32_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream) {
+  return sort_impl(reinterpret_cast<uint32_t*>(d_keys), n, 1, descending,
+                   0x80000000u, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_u32_batched(uint32_t* d_keys, uint64_t n_per_array,
+                                  uint64_t batch, int descending,
+                                  b200_stream_t stream) {
+  return sort_impl(d_keys, n_per_array, batch, descending, 0u,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_i32_batched(int32_t* d_keys, uint64_t n_per_array,
+                                  uint64_t batch, int descending,
+                                  b200_stream_t stream) {
+  return sort_impl(reinterpret_cast<uint32_t*>(d_keys), n_per_array, batch,
+                   descending, 0x80000000u,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+static int host_sort(uint32_t* h, uint64_t n, int descending, uint32_t key_xor) {
+  if (n < 2 || !is_pow2(n)) {
+    return fail(B200_INVALID_SIZE,
+                "length must be a power of two >= 2, got " + std::to_string(n));
+  }
+  if (h == nullptr) return fail(B200_CONFIG, "null key pointer");
+  uint32_t* d = nullptr;
+  cudaStream_t s = nullptr;
+  B200_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMallocAsync(&d, n * 4, s);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(s);
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  int rc = B200_OK;
+  e = cudaMemcpyAsync(d, h, n * 4, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) rc = cuda_fail(e, "H2D copy");
+  if (rc == B200_OK) rc = sort_impl(d, n, 1, descending, key_xor, s);
+  if (rc == B200_OK) {
+    e = cudaMemcpyAsync(h, d, n * 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
+  }
+  cudaFreeAsync(d, s);
+  e = cudaStreamSynchronize(s);
+  if (rc == B200_OK && e != cudaSuccess) rc = cuda_fail(e, "sort");
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending) {
+  return host_sort(reinterpret_cast<uint32_t*>(h_keys), n, descending,
+                   0x80000000u);
+}
+
+int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending) {
+  return host_sort(h_keys, n, descending, 0u);
+}
+
+int b200_bitonic_merge_split_u32(const uint32_t* local, const uint32_t* partner,
+                                 uint64_t m, int keep_high, uint32_t key_xor,
+                                 uint32_t* out, b200_stream_t stream) {
+  if (m < 1) return fail(B200_INVALID_SIZE, "shard must hold >= 1 key");
+  if (!local || !partner || !out) return fail(B200_CONFIG, "null pointer");
+  if (out == local || out == partner) {
+    return fail(B200_CONFIG, "out must not alias the inputs");
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t tiles = (m + b200::kMergeTile - 1) / b200::kMergeTile;
+  uint64_t* cor = nullptr;
+  B200_CUDA_TRY(cudaMallocAsync(&cor, (tiles + 1) * sizeof(uint64_t), s));
+  int rc = merge_split_impl(local, partner, m, keep_high, key_xor, out, cor, s);
+  cudaFreeAsync(cor, s);
+  return rc;
+}
+
+// Rank-level bitonic network over G sorted shards (block bitonic sort with
+// merge-split compare-exchanges).  Same direction rule as the reference's
+// network (schedule.cpp:58-67) applied to shard indices.
+int b200_bitonic_sort_u32_multi(uint32_t* const* d_shards, const int* devices,
+                                int ngpu, uint64_t n_total, int descending) {
+  if (ngpu != 1 && ngpu != 2 && ngpu != 4 && ngpu != 8) {
+    return fail(B200_CONFIG, "ngpu must be 1, 2, 4 or 8");
+  }
+  if (!d_shards || !devices) return fail(B200_CONFIG, "null pointer");
+  if (n_total < 2 || !is_pow2(n_total) || n_total < (uint64_t)ngpu * 2) {
+    return fail(B200_INVALID_SIZE,
+                "n_total must be a power of two >= 2*ngpu");
+  }
+  if (descending != 0 && descending != 1) {
+    return fail(B200_CONFIG, "descending must be 0 or 1");
+  }
+  const uint64_t m = n_total / ngpu;
+  const uint32_t gmask = descending ? 0xFFFFFFFFu : 0u;
+  int prev_dev = 0;
+  B200_CUDA_TRY(cudaGetDevice(&prev_dev));
+
+  // Enable peer access between distinct devices.
+  for (int r = 0; r < ngpu; ++r) {
+    for (int q = 0; q < ngpu; ++q) {
+      if (devices[r] == devices[q]) continue;
+      int can = 0;
+      B200_CUDA_TRY(cudaDeviceCanAccessPeer(&can, devices[r], devices[q]));
+      if (!can) {
+        cudaSetDevice(prev_dev);
+        return fail(B200_CONFIG, "no peer access between devices");
+      }
+      B200_CUDA_TRY(cudaSetDevice(devices[r]));
+      cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        cudaSetDevice(prev_dev);
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  }
+
+  std::vector<cudaStream_t> st(ngpu, nullptr);
+  std::vector<cudaEvent_t> ev(ngpu, nullptr);
+  std::vector<uint32_t*> cur(d_shards, d_shards + ngpu), tmp(ngpu, nullptr);
+  std::vector<uint32_t*> scratch(ngpu, nullptr);
+  std::vector<uint64_t*> cor(ngpu, nullptr);
+  const uint64_t tiles = (m + b200::kMergeTile - 1) / b200::kMergeTile;
+  int rc = B200_OK;
+  auto cleanup = [&]() {
+    for (int r = 0; r < ngpu; ++r) {
+      cudaSetDevice(devices[r]);
+      if (st[r]) cudaStreamSynchronize(st[r]);
+      if (scratch[r]) cudaFree(scratch[r]);
+      if (cor[r]) cudaFree(cor[r]);
+      if (ev[r]) cudaEventDestroy(ev[r]);
+      if (st[r]) cudaStreamDestroy(st[r]);
+    }
+    cudaSetDevice(prev_dev);
+  };
+#define MTRY(expr)                                   \
+  do {                                               \
+    cudaError_t _e = (expr);                         \
+    if (_e != cudaSuccess) {                         \
+      rc = cuda_fail(_e, #expr);                     \
+      cleanup();                                     \
+      return rc;                                     \
+    }                                                \
+  } while (0)
+
+  for (int r = 0; r < ngpu; ++r) {
+    MTRY(cudaSetDevice(devices[r]));
+    MTRY(cudaStreamCreateWithFlags(&st[r], cudaStreamNonBlocking));
+    MTRY(cudaEventCreateWithFlags(&ev[r], cudaEventDisableTiming));
+    if (ngpu > 1) {
+      MTRY(cudaMalloc(&scratch[r], m * 4));
+      tmp[r] = scratch[r];
+      MTRY(cudaMalloc(&cor[r], (tiles + 1) * sizeof(uint64_t)));
+    }
+  }
+  // 1. local sorts (each shard ascending in the requested order)
+  for (int r = 0; r < ngpu; ++r) {
+    MTRY(cudaSetDevice(devices[r]));
+    rc = sort_impl(cur[r], m, 1, descending, 0u, st[r]);
+    if (rc != B200_OK) {
+      std::string msg = g_last_error;
+      cleanup();
+      g_last_error = msg;
+      return rc;
+    }
+  }
+  // 2. rank-level network: phases q = 1..g, steps s = q..1
+  int g = 0;
+  while ((1 << g) < ngpu) ++g;
+  for (int q = 1; q <= g; ++q) {
+    for (int s = q; s >= 1; --s) {
+      for (int r = 0; r < ngpu; ++r) {
+        MTRY(cudaSetDevice(devices[r]));
+        MTRY(cudaEventRecord(ev[r], st[r]));
+      }
+      for (int r = 0; r < ngpu; ++r) {
+        const int partner = r ^ (1 << (s - 1));
+        MTRY(cudaSetDevice(devices[r]));
+        MTRY(cudaStreamWaitEvent(st[r], ev[partner], 0));
+        const bool ascending = ((r >> q) & 1) == 0;
+        const bool lower = r < partner;
+        const int keep_high = (lower == ascending) ? 0 : 1;
+        rc = merge_split_impl(cur[r], cur[partner], m, keep_high, gmask,
+                              tmp[r], cor[r], st[r]);
+        if (rc != B200_OK) {
+          std::string msg = g_last_error;
+          cleanup();
+          g_last_error = msg;
+          return rc;
+        }
+      }
+      // both halves of every pair must finish reading before buffers swap
+      for (int r = 0; r < ngpu; ++r) {
+        MTRY(cudaSetDevice(devices[r]));
+        MTRY(cudaEventRecord(ev[r], st[r]));
+      }
+      for (int r = 0; r < ngpu; ++r) {
+        const int partner = r ^ (1 << (s - 1));
+        MTRY(cudaSetDevice(devices[r]));
+        MTRY(cudaStreamWaitEvent(st[r], ev[partner], 0));
+      }
+      std::swap(cur, tmp);
+    }
+  }
+  // 3. results must end in the caller's buffers
+  for (int r = 0; r < ngpu; ++r) {
+    if (cur[r] != d_shards[r]) {
+      MTRY(cudaSetDevice(devices[r]));
+      MTRY(cudaMemcpyAsync(d_shards[r], cur[r], m * 4, cudaMemcpyDeviceToDevice,
+                           st[r]));
+    }
+  }
+  for (int r = 0; r < ngpu; ++r) {
+    MTRY(cudaSetDevice(devices[r]));
+    MTRY(cudaStreamSynchronize(st[r]));
+  }
+  cleanup();
+#undef MTRY
+  return B200_OK;
+}
+
+int b200_bitonic_plan(uint64_t n, uint64_t batch, b200_pass_info* out,
+                      int max_passes, int* n_passes) {
+  if (n < 2 || !is_pow2(n)) {
+    return fail(B200_INVALID_SIZE,
+                "length must be a power of two >= 2, got " + std::to_string(n));
+  }
+  if (batch < 1) return fail(B200_CONFIG, "batch must be >= 1");
+  std::vector<b200::PlanPass> plan;
+  try {
+    plan = b200::make_plan(log2_exact(n), batch, plan_options());
+  } catch (const std::exception& e) {
+    return fail(B200_CONFIG, e.what());
+  }
+  if (n_passes) *n_passes = (int)plan.size();
+  for (int i = 0; i < (int)plan.size() && i < max_passes && out; ++i) {
+    const auto& q = plan[i];
+    out[i].tile_bits = q.C;
+    out[i].a = q.a;
+    out[i].y = q.y;
+    out[i].tile_sort = q.tile_sort;
+    out[i].segA_hi = q.segA_hi;
+    out[i].pA = q.tile_sort ? q.p_end : q.pA;
+    out[i].segB_lo = q.segB_lo;
+    out[i].pB = q.pB;
+    out[i].ctas = q.ctas;
+    out[i].compare_exchanges = q.ces;
+  }
+  return B200_OK;
+}
+
+int b200_bitonic_counters(uint64_t n, uint64_t batch, uint64_t out[4]) {
+  int np = 0;
+  int rc = b200_bitonic_plan(n, batch, nullptr, 0, &np);
+  if (rc) return rc;
+  std::vector<b200_pass_info> v(np);
+  b200_bitonic_plan(n, batch, v.data(), np, &np);
+  uint64_t ces = 0;
+  for (auto& p : v) ces += p.compare_exchanges;
+  out[0] = (uint64_t)np;
+  out[1] = (uint64_t)np * n * batch;
+  out[2] = (uint64_t)np * n * batch;
+  out[3] = ces;
+  return B200_OK;
+}
+
+int b200_bitonic_set_tuning(int tile_bits, int min_run_bits) {
+  if (tile_bits != 0 && (tile_bits < 6 || tile_bits > b200::kMaxTileBits)) {
+    return fail(B200_CONFIG, "tile_bits must be 0 (auto) or in [6, 15]");
+  }
+  if (min_run_bits < 2 || min_run_bits > 10) {
+    return fail(B200_CONFIG, "min_run_bits must be in [2, 10]");
+  }
+  g_tile_bits.store(tile_bits);
+  g_min_run_bits.store(min_run_bits);
+  return B200_OK;
+}
+
+const char* b200_bitonic_last_error(void) { return g_last_error.c_str(); }
+
+const char* b200_bitonic_version(void) { return "b200-bitonic 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// planner.hpp -- host-side pass planner for the bitonic network.
+//
+// Generalises the reference's build_plan (proj/src/engine.cpp:86-145).  The
+// reference packs the schedule (generate_schedule, schedule.cpp:20-36: phase
+// p = 1..k, steps on bits p-1..0) into launches of three fixed kinds: one
+// step, two paired steps, or the block-local tail of one phase.  Here a
+// launch ("pass") may cover ANY run of consecutive steps whose bits fit in a
+// C-bit coset S = [0,a) U [y, y+C-a) of the index space, so one HBM round
+// trip covers up to C steps:
+//   * pass 0 (tile sort): phases 1..C of every 2^C tile;
+//   * merge passes, greedily: the tail of phase p (bits b..0, all < C) fused
+//     with the head of phase p+1 (bits p..p-h+1), or, when a phase has too
+//     many bits, a middle run of h = C - lrun high bits.
+// Every pass keeps at least 2^lrun contiguous keys per run (lrun >= 2 so the
+// kernels use 128-bit accesses; 5 = one 128 B line).  Concatenating the
+// passes' steps reproduces the schedule's step order exactly -- the same
+// invariant the reference tests for its plans (test_engine.cpp:99-118) -- and
+// the CE total equals predicted_counts (schedule.cpp:71-78).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace b200 {
+
+struct PlanPass {
+  int C = 0;          // tile bits
+  int a = 0, y = 0;   // coset shape
+  int tile_sort = 0;  // phases 1..p_end in one tile
+  int p_end = 0;      // last phase of a tile-sort pass
+  int segA_hi = -1, pA = 0;
+  int segB_lo = -1, pB = 0;
+  uint64_t ctas = 0;
+  uint64_t ces = 0;
+};
+
+struct PlanOptions {
+  int cmax = 14;   // largest tile (2^cmax keys per CTA)
+  int lrun = 5;    // min contiguous run per merge pass (2^lrun keys)
+  int min_ctas = 128;  // shrink the tile until the grid has this many CTAs
+  int cmin = 10;   // ... but not below this tile size
+};
+
+inline int ctz64(uint64_t x) {
+  int r = 0;
+  while (!(x & 1ull)) {
+    x >>= 1;
+    ++r;
+  }
+  return r;
+}
+
+// One entry per steps-run, in execution order.  k = log2(keys per array),
+// batch = number of contiguous arrays (each sorted independently).
+inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
+                                       const PlanOptions& opt) {
+  if (k < 1 || k > 40) throw std::invalid_argument("k out of range");
+  if (batch < 1) throw std::invalid_argument("batch must be >= 1");
+  const uint64_t total = batch << k;
+  const int kt = k + ctz64(batch);  // tiles must divide the whole buffer
+  std::vector<PlanPass> plan;
+
+  // Tile size: as large as allowed, shrunk for small problems so the grid
+  // still covers the SMs.
+  int C = opt.cmax;
+  if (k <= 15 && k > C) C = k;  // one array fits one CTA: a single launch
+  if (C > kt) C = kt;
+  // Shrink the tile for small problems so the grid still covers the SMs --
+  // but never below k when the whole array fits one tile (that would add
+  // merge passes).
+  while (C > opt.cmin && C > k && (total >> C) < (uint64_t)opt.min_ctas) --C;
+  if (k > C) {
+    while (C > opt.cmin && (total >> C) < (uint64_t)opt.min_ctas) --C;
+  }
+  // Merge passes need a coalescing run below the high range and a phase
+  // direction bit that is per-thread uniform in layout L_0 (C - 1 >= 5).
+  if (k > C && C < opt.lrun + 1) C = opt.lrun + 1;
+  if (k > C && C < 6) C = 6;
+  if (C > kt) C = kt;
+
+  PlanPass t;
+  t.C = C;
+  t.a = C;
+  t.y = C;
+  t.tile_sort = 1;
+  t.p_end = k < C ? k : C;
+  t.ctas = total >> C;
+  t.ces = (total / 2) * (uint64_t)(t.p_end * (t.p_end + 1) / 2);
+  plan.push_back(t);
+  if (k <= C) return plan;
+
+  const int lrun = opt.lrun;
+  int p = C + 1;  // current phase
+  int b = C;      // next step bit of phase p (steps run b, b-1, ..., 0)
+  while (p <= k) {
+    PlanPass m;
+    m.C = C;
+    m.ctas = total >> C;
+    if (b < C) {
+      // Tail of phase p fits in the low bits: fuse the head of phase p+1.
+      const int low = (b + 1 > lrun) ? b + 1 : lrun;
+      int h = C - low;
+      if (p == k) h = 0;
+      m.segA_hi = b;
+      m.pA = p;
+      if (h > 0) {
+        m.a = C - h;
+        m.y = p - h + 1;
+        m.segB_lo = m.a;
+        m.pB = p + 1;
+        m.ces = (total / 2) * (uint64_t)((b + 1) + h);
+        plan.push_back(m);
+        b = p - h;  // next step bit of phase p+1
+        p = p + 1;
+      } else {
+        m.a = C;
+        m.y = C;
+        m.ces = (total / 2) * (uint64_t)(b + 1);
+        plan.push_back(m);
+        p = p + 1;
+        b = p - 1;
+      }
+    } else {
+      // Middle of phase p: h high bits b..b-h+1 plus a coalescing run.
+      int h = C - lrun;
+      // Do not take more than leaves a non-empty remainder.
+      if (h > b) h = b;
+      m.a = C - h;
+      m.y = b - h + 1;
+      m.segB_lo = m.a;
+      m.pB = p;
+      m.ces = (total / 2) * (uint64_t)h;
+      plan.push_back(m);
+      b -= h;
+    }
+  }
+  return plan;
+}
+
+}  // namespace b200
