@@ -1,10 +1,12 @@
 """Build the in-tree sm_100a shared library (libb200_bitonic.so).
 
 nvcc cross-compiles for sm_100a without a GPU; the .so is git-ignored but
-travels to the GPU box with the repo snapshot.
+travels to the GPU box with the repo snapshot.  The specialised kernels are
+split over several translation units that compile in parallel.
 """
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import shutil
 import subprocess
@@ -12,17 +14,18 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libb200_bitonic.so")
-SOURCES = [os.path.join(CSRC, "bitonic_sort.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
+SOURCES = [os.path.join(CSRC, f) for f in
+           ["bitonic_sort.cu", "k_tile.cu", "k_merge11.cu", "k_merge12.cu",
+            "k_merge13.cu", "k_merge14.cu", "k_merge15.cu"]]
+HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
+           if f.endswith((".cuh", ".hpp", ".h"))]
 HEADERS.append(os.path.join(ROOT, "include", "b200_bitonic.h"))
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-Xptxas", "-warn-spills",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                     "-Xptxas", "-warn-spills"]
 
 
 def nvcc() -> str:
@@ -32,20 +35,44 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def needs_build() -> bool:
+    return _stale(LIB, SOURCES + HEADERS)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB, *SOURCES]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    os.makedirs(OBJ, exist_ok=True)
+    nv = nvcc()
+    jobs = []
+    for src in SOURCES:
+        obj = _obj(src)
+        if force or _stale(obj, [src] + HEADERS):
+            jobs.append([nv, *NVCC_FLAGS, "-c", "-o", obj, src])
+
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        if verbose and (r.stdout or r.stderr):
+            print(r.stdout + r.stderr, flush=True)
+
+    with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4) or 1) as ex:
+        list(ex.map(run, jobs))
+    run([nv, *ARCH, "-shared", "-o", LIB, *[_obj(s) for s in SOURCES]])
     return LIB
 
 

@@ -19,6 +19,7 @@
 
 #include "../../include/b200_bitonic.h"
 #include "bitonic_engine.cuh"
+#include "kernel_tables.hpp"
 #include "merge_split.cuh"
 #include "planner.hpp"
 
@@ -64,63 +65,75 @@ int log2_exact(uint64_t n) {
 
 bool is_pow2(uint64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
 
-// ---- per-device kernel attributes (max dynamic shared memory) -----------
+// ---- kernel selection and launch --------------------------------------------
+// Specialised (compile-time step sequence) kernels are used for every pass
+// shape that was instantiated; anything else runs on the runtime-dispatched
+// bitonic_pass_kernel<C>.  Both are sm_100a code; there is no host fallback.
 template <int C>
-cudaError_t set_attrs() {
-  const int bytes = b200::tile_smem_words(C) * 4;
-  if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(b200::bitonic_pass_kernel<C>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              bytes);
+b200::PassFn generic_kernel_c() {
+  return &b200::bitonic_pass_kernel<C>;
 }
 
-std::mutex g_attr_mu;
-std::vector<int> g_attr_done;
+b200::PassFn generic_kernel(int C) {
+  switch (C) {
+    case 1: return generic_kernel_c<1>();
+    case 2: return generic_kernel_c<2>();
+    case 3: return generic_kernel_c<3>();
+    case 4: return generic_kernel_c<4>();
+    case 5: return generic_kernel_c<5>();
+    case 6: return generic_kernel_c<6>();
+    case 7: return generic_kernel_c<7>();
+    case 8: return generic_kernel_c<8>();
+    case 9: return generic_kernel_c<9>();
+    case 10: return generic_kernel_c<10>();
+    case 11: return generic_kernel_c<11>();
+    case 12: return generic_kernel_c<12>();
+    case 13: return generic_kernel_c<13>();
+    case 14: return generic_kernel_c<14>();
+    default: return generic_kernel_c<15>();
+  }
+}
 
-cudaError_t ensure_attrs() {
+std::atomic<int> g_force_generic{0};
+
+b200::PassFn select_kernel(const b200::PlanPass& q) {
+  if (!g_force_generic.load()) {
+    b200::PassFn f = q.tile_sort ? b200::find_tile_kernel(q.C)
+                                 : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo);
+    if (f) return f;
+  }
+  return generic_kernel(q.C);
+}
+
+// Max-dynamic-shared-memory attribute, set once per (device, kernel).
+std::mutex g_attr_mu;
+std::vector<std::vector<const void*>> g_attr_done;
+
+cudaError_t ensure_attr(const void* fn, int C) {
+  const int bytes = b200::tile_smem_words(C) * 4;
+  if (bytes <= 48 * 1024) return cudaSuccess;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  if ((int)g_attr_done.size() <= dev) g_attr_done.resize(dev + 1, 0);
-  if (g_attr_done[dev]) return cudaSuccess;
-  cudaError_t r = cudaSuccess;
-  auto chk = [&](cudaError_t x) { if (r == cudaSuccess && x != cudaSuccess) r = x; };
-  chk(set_attrs<11>());
-  chk(set_attrs<12>());
-  chk(set_attrs<13>());
-  chk(set_attrs<14>());
-  chk(set_attrs<15>());
-  if (r == cudaSuccess) g_attr_done[dev] = 1;
-  return r;
+  if ((int)g_attr_done.size() <= dev) g_attr_done.resize(dev + 1);
+  auto& done = g_attr_done[dev];
+  if (std::find(done.begin(), done.end(), fn) != done.end()) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back(fn);
+  return e;
 }
 
-template <int C>
-void launch_c(const b200::PassParams& p, uint64_t ctas, cudaStream_t s) {
-  constexpr int T = b200::tile_threads(C);
-  const size_t smem = (size_t)b200::tile_smem_words(C) * 4;
-  b200::bitonic_pass_kernel<C><<<(unsigned)ctas, T, smem, s>>>(p);
-}
-
-void launch_pass(int C, const b200::PassParams& p, uint64_t ctas,
-                 cudaStream_t s) {
-  switch (C) {
-    case 1: launch_c<1>(p, ctas, s); break;
-    case 2: launch_c<2>(p, ctas, s); break;
-    case 3: launch_c<3>(p, ctas, s); break;
-    case 4: launch_c<4>(p, ctas, s); break;
-    case 5: launch_c<5>(p, ctas, s); break;
-    case 6: launch_c<6>(p, ctas, s); break;
-    case 7: launch_c<7>(p, ctas, s); break;
-    case 8: launch_c<8>(p, ctas, s); break;
-    case 9: launch_c<9>(p, ctas, s); break;
-    case 10: launch_c<10>(p, ctas, s); break;
-    case 11: launch_c<11>(p, ctas, s); break;
-    case 12: launch_c<12>(p, ctas, s); break;
-    case 13: launch_c<13>(p, ctas, s); break;
-    case 14: launch_c<14>(p, ctas, s); break;
-    default: launch_c<15>(p, ctas, s); break;
-  }
+cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
+                        cudaStream_t s) {
+  b200::PassFn f = select_kernel(q);
+  const void* fn = reinterpret_cast<const void*>(f);
+  cudaError_t e = ensure_attr(fn, q.C);
+  if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)b200::tile_smem_words(q.C) * 4;
+  void* args[] = {&p};
+  return cudaLaunchKernel(fn, dim3((unsigned)q.ctas), dim3(b200::tile_threads(q.C)),
+                          args, smem, s);
 }
 
 // Validates and runs the whole plan.  key_xor: 0x80000000 for int32 keys.
@@ -149,7 +162,6 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
   if (plan.front().C >= 2 && (reinterpret_cast<uintptr_t>(d_keys) & 15u) != 0) {
     return fail(B200_CONFIG, "device pointer must be 16-byte aligned");
   }
-  B200_CUDA_TRY(ensure_attrs());
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
   for (size_t i = 0; i < plan.size(); ++i) {
     const b200::PlanPass& q = plan[i];
@@ -166,9 +178,9 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     p.pA = q.pA;
     p.segB_lo = q.segB_lo;
     p.pB = q.pB;
-    launch_pass(q.C, p, q.ctas, stream);
+    cudaError_t e = launch_pass(q, p, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "bitonic pass launch");
   }
-  B200_CUDA_TRY(cudaGetLastError());
   return B200_OK;
 }
 
@@ -465,6 +477,10 @@ int b200_bitonic_counters(uint64_t n, uint64_t batch, uint64_t out[4]) {
 }
 
 int b200_bitonic_set_tuning(int tile_bits, int min_run_bits) {
+  // min_run_bits >= 100 selects the runtime-dispatched kernels (testing aid):
+  // b200_bitonic_set_tuning(t, 100 + r) == (t, r) with generic kernels.
+  g_force_generic.store(min_run_bits >= 100 ? 1 : 0);
+  if (min_run_bits >= 100) min_run_bits -= 100;
   if (tile_bits != 0 && (tile_bits < 6 || tile_bits > b200::kMaxTileBits)) {
     return fail(B200_CONFIG, "tile_bits must be 0 (auto) or in [6, 15]");
   }

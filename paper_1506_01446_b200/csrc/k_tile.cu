@@ -1,0 +1,55 @@
+// k_tile.cu -- tile-sort kernels (all tile sizes) and the table lookups.
+#include "bitonic_static.cuh"
+#include "kernel_tables.hpp"
+
+namespace b200 {
+
+PassFn find_tile_kernel(int C) {
+  switch (C) {
+    case 1: return &tile_sort_kernel<1>;
+    case 2: return &tile_sort_kernel<2>;
+    case 3: return &tile_sort_kernel<3>;
+    case 4: return &tile_sort_kernel<4>;
+    case 5: return &tile_sort_kernel<5>;
+    case 6: return &tile_sort_kernel<6>;
+    case 7: return &tile_sort_kernel<7>;
+    case 8: return &tile_sort_kernel<8>;
+    case 9: return &tile_sort_kernel<9>;
+    case 10: return &tile_sort_kernel<10>;
+    case 11: return &tile_sort_kernel<11>;
+    case 12: return &tile_sort_kernel<12>;
+    case 13: return &tile_sort_kernel<13>;
+    case 14: return &tile_sort_kernel<14>;
+    case 15: return &tile_sort_kernel<15>;
+    default: return nullptr;
+  }
+}
+
+namespace {
+struct Tables {
+  MergeTable t[kMergeCMax + 1];
+  Tables() {
+    for (auto& x : t) x = MergeTable{};
+    fill_merge_table_11(t[11]);
+    fill_merge_table_12(t[12]);
+    fill_merge_table_13(t[13]);
+    fill_merge_table_14(t[14]);
+    fill_merge_table_15(t[15]);
+  }
+};
+const Tables& tables() {
+  static Tables tb;
+  return tb;
+}
+}  // namespace
+
+PassFn find_merge_kernel(int C, int SA, int SB) {
+  if (C < kMergeCMin || C > kMergeCMax) return nullptr;
+  const MergeTable& t = tables().t[C];
+  if (SB >= 0 && SA == SB - 1 && SB < 16) return t.th[SB];
+  if (SA < 0 && SB >= 0 && SB < 16) return t.ho[SB];
+  if (SB < 0 && SA >= 0 && SA < 16) return t.to[SA];
+  return nullptr;
+}
+
+}  // namespace b200

@@ -1,0 +1,33 @@
+// kernel_tables.hpp -- lookup of the compile-time specialised pass kernels.
+#pragma once
+
+#include "bitonic_engine.cuh"
+
+namespace b200 {
+
+using PassFn = void (*)(PassParams);
+
+// Tile-sort kernel for a 2^C tile (C in [1, 15]).
+PassFn find_tile_kernel(int C);
+// Specialised merge kernel for local bits SA..0 then C-1..SB, or nullptr when
+// that shape was not instantiated (the caller then uses the runtime-dispatched
+// bitonic_pass_kernel<C>).
+PassFn find_merge_kernel(int C, int SA, int SB);
+
+// Instantiated merge tile sizes.
+constexpr int kMergeCMin = 11;
+constexpr int kMergeCMax = 15;
+
+struct MergeTable {
+  PassFn th[16];  // SA = A-1, SB = A   (tail + head),  A in [2, C-1]
+  PassFn ho[16];  // SA = -1,  SB = A   (head only),    A in [2, C-1]
+  PassFn to[16];  // SA,       SB = -1  (tail only),    SA in [0, C-1]
+};
+
+void fill_merge_table_11(MergeTable& t);
+void fill_merge_table_12(MergeTable& t);
+void fill_merge_table_13(MergeTable& t);
+void fill_merge_table_14(MergeTable& t);
+void fill_merge_table_15(MergeTable& t);
+
+}  // namespace b200
