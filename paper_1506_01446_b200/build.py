@@ -24,7 +24,7 @@ HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
 HEADERS.append(os.path.join(ROOT, "include", "b200_bitonic.h"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills"]
 
 

@@ -48,9 +48,15 @@ constexpr int kMaxTileBits = 15;
 __host__ __device__ constexpr int reg_bits(int C) {
   return C < kRegBits ? C : kRegBits;
 }
+// Shared-memory padding: pad(j) = j + j/32 + j/1024.  Additive over
+// disjoint bit fields (so register addresses are immediates), and for any 5
+// lane bits with distinct residues mod 5 the 32 lanes hit 32 distinct banks.
+__host__ __device__ constexpr uint32_t smem_pad(uint32_t j) {
+  return j + (j >> 5) + (j >> 10);
+}
 // Padded shared-memory words for a 2^C tile.
 __host__ __device__ constexpr int tile_smem_words(int C) {
-  return (1 << C) + ((1 << C) >> 5);
+  return (int)smem_pad((1u << C) - 1u) + 1;
 }
 __host__ __device__ constexpr int tile_threads(int C) {
   return 1 << (C - reg_bits(C));
@@ -94,7 +100,7 @@ struct Tile {
   }
 
   __device__ __forceinline__ static uint32_t pad(uint32_t j) {
-    return j + (j >> 5);
+    return smem_pad(j);
   }
   template <int Z>
   __device__ __forceinline__ static uint32_t spread(uint32_t t) {
@@ -114,13 +120,13 @@ struct Tile {
   __device__ __forceinline__ static void sts(uint32_t* sm, const uint32_t (&v)[NR]) {
     const uint32_t b = base_addr<Z>();
 #pragma unroll
-    for (int e = 0; e < NR; ++e) sm[b + (((uint32_t)e << Z) + (((uint32_t)e << Z) >> 5))] = v[e];
+    for (int e = 0; e < NR; ++e) sm[b + smem_pad((uint32_t)e << Z)] = v[e];
   }
   template <int Z>
   __device__ __forceinline__ static void lds(const uint32_t* sm, uint32_t (&v)[NR]) {
     const uint32_t b = base_addr<Z>();
 #pragma unroll
-    for (int e = 0; e < NR; ++e) v[e] = sm[b + (((uint32_t)e << Z) + (((uint32_t)e << Z) >> 5))];
+    for (int e = 0; e < NR; ++e) v[e] = sm[b + smem_pad((uint32_t)e << Z)];
   }
   __device__ __forceinline__ static void sts_layout(int L, uint32_t* sm, const uint32_t (&v)[NR]) {
     if (L == 0) sts<Z0>(sm, v);

@@ -98,8 +98,9 @@ std::atomic<int> g_force_generic{0};
 
 b200::PassFn select_kernel(const b200::PlanPass& q) {
   if (!g_force_generic.load()) {
-    b200::PassFn f = q.tile_sort ? b200::find_tile_kernel(q.C)
-                                 : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo);
+    b200::PassFn f = q.tile_sort
+                         ? (q.p_end == q.C ? b200::find_tile_kernel(q.C) : nullptr)
+                         : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo);
     if (f) return f;
   }
   return generic_kernel(q.C);

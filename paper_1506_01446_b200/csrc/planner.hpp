@@ -66,6 +66,9 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // still covers the SMs.
   int C = opt.cmax;
   if (k <= 15 && k > C) C = k;  // one array fits one CTA: a single launch
+  // Batched arrays of >= 2^8 keys: one array per CTA (the specialised tile
+  // sort runs exactly phases 1..C).  Smaller arrays share a tile.
+  if (batch > 1 && k >= 8 && k <= 15) C = k;
   if (C > kt) C = kt;
   // Shrink the tile for small problems so the grid still covers the SMs --
   // but never below k when the whole array fits one tile (that would add
