@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""bench.py -- device-timed Gkeys/s of the B200 bitonic sort (BASELINE.json metric).
+
+Default (N=1): BASELINE.json configs[1], 2^20 random uint32 keys on one B200,
+ascending.  One "step" = one full sort of the 2^20-key array.  The unsorted
+input is restored (device-to-device copy) and L2 is flushed (a 256 MiB write,
+larger than the 126 MB L2) before every step, outside the timed region; each
+step is timed with CUDA events on the sorting stream and the K durations are
+summed.  Under torchrun (N>1) every rank owns a 2^20-key shard of one
+N*2^20-key array and the partitioned sort (local sort + NCCL merge-split
+network, paper_1506_01446_b200/dist.py) is timed, max over ranks ("weak").
+
+Extra JSON keys (see the task contract): e2e (host pinned buffers, H2D + sort
++ D2H inside the timed region), roofline (dominant kernel family, measured
+live with CUDA events per launch), sort_roofline (north_star's whole-sort
+definition: P_min x 8 bytes x n / HBM BW), cpu_baseline (the reference's own
+CPU code from oracle/_ref, timed on this host), clocks (nvidia-smi sampled
+during the timed region), gpu_launches.
+
+``--impl reference`` times the reference's CPU implementation of the path
+(oracle/_ref: bitonic::execute(build_plan(fused, 1024)) on all host threads)
+on the same workload and prints the same line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+METRIC = "Gkeys/s sorting uint32 (device-timed) vs HBM roofline; speedup vs CPU quicksort"
+# P_min(k, c=15): minimum HBM round trips of the network.
+PMIN = {16: 3, 20: 7, 24: 13, 28: 21, 29: 22, 30: 24, 31: 27, 32: 29}
+
+
+def pmin(k: int, c: int = 15) -> int:
+    if k in PMIN:
+        return PMIN[k]
+    bits, passes = set(), 1
+    for p in range(1, k + 1):
+        for s in range(p, 0, -1):
+            nb = bits | {s - 1}
+            if len(nb) > c:
+                passes += 1
+                nb = {s - 1}
+            bits = nb
+    return passes
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return HBM_FALLBACK, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU): the reference's own code from oracle/_ref
+# ---------------------------------------------------------------------------
+def reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    ref = oracle.reference()
+    n = 1 << args.log2n
+    cores = os.cpu_count() or 1
+    if ref is not None:
+        kind = "reference"
+        rng = np.random.default_rng(1)
+        x = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+        work = x.copy()
+        run = lambda: ref.execute_inplace(work, 2, min(1024, n), cores)
+        what = f"bitonic::execute(build_plan(fused, {min(1024, n)}), keys, {cores} workers)"
+    else:  # pragma: no cover - oracle port when the reference was not built
+        kind = "port"
+        o = oracle.oracle()
+        x = o.generate_input(n, 1).view(np.int32)
+        work = x.copy()
+        run = lambda: work.__setitem__(slice(None), o.sequential_bitonic_i32(work))
+        what = "oracle sequential_bitonic_i32 (1 core)"
+        cores = 1
+    for _ in range(args.warmup):
+        work[:] = x
+        run()
+    times = []
+    for _ in range(args.steps):
+        work[:] = x
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    assert (np.diff(work.astype(np.int64)) >= 0).all()
+    ms = 1e3 * sum(times) / len(times)
+    value = n / (ms * 1e-3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gkeys/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"2^{args.log2n} random uint32 keys, ascending (CPU)",
+                   "keys": n},
+        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": cores,
+                         "kind": kind, "sample": what},
+        "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(n: int, budget_s: float = 12.0):
+    """The paper's CPU quicksort and the reference's CPU bitonic sorts, timed
+    on this host on the same workload (oracle/_ref = the reference's code)."""
+    import numpy as np
+    import oracle
+    ref = oracle.reference()
+    rng = np.random.default_rng(1)
+    x = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    cores = os.cpu_count() or 1
+    out = {}
+    if ref is None:
+        o = oracle.oracle()
+        kind, qs = "port", (lambda a: a.__setitem__(slice(None), o.quicksort_i32(a)))
+        seq = lambda a: a.__setitem__(slice(None), o.sequential_bitonic_i32(a))
+        fused = None
+    else:
+        kind = "reference"
+        qs = ref.quicksort_inplace
+        seq = ref.sequential_bitonic_sort_inplace
+        fused = lambda a: ref.execute_inplace(a, 2, min(1024, n), cores)
+    t_start = time.perf_counter()
+
+    def best(fn, reps):
+        b = float("inf")
+        for _ in range(reps):
+            w = x.copy()
+            t0 = time.perf_counter()
+            fn(w)
+            b = min(b, time.perf_counter() - t0)
+            if time.perf_counter() - t_start > budget_s:
+                break
+        return b
+
+    out["quicksort_ms"] = 1e3 * best(qs, 5)
+    out["sequential_bitonic_ms"] = 1e3 * best(seq, 3)
+    if fused is not None:
+        out["fused_engine_ms"] = 1e3 * best(fused, 3)
+    return kind, cores, out
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log2n", type=int, default=20,
+                    help="keys per GPU = 2^log2n (default 20 = BASELINE configs[1])")
+    ap.add_argument("--batched", type=int, default=0,
+                    help="n_per_array for the batched config (e.g. 4096)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1506_01446_b200 as b200
+
+    world, rank, local = dist_env()
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    n = 1 << args.log2n
+    hbm, peak_kind, peaks_json = peaks()
+    g = torch.Generator(device=dev)
+    g.manual_seed(1 + rank)
+    src = torch.randint(-2**31, 2**31, (n,), dtype=torch.int64, device=dev,
+                        generator=g).to(torch.int32).view(torch.uint32)
+    work = src.clone()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    batched = args.batched
+    if world > 1:
+        from paper_1506_01446_b200 import dist as bdist
+        ops = bdist.cuda_ops()
+
+        def sort_step():
+            bdist.partitioned_sort_(work, ops=ops)
+        plan = b200.plan(n)
+        launches_per_step = len(plan) + 2 * len(bdist.network_steps(world))
+        workload = (f"{world}x2^{args.log2n} random uint32 keys, one array partitioned "
+                    f"over {world} GPUs (local sort + NCCL merge-split network)")
+    elif batched:
+        def sort_step():
+            b200.sort_batched_(work, batched)
+        plan = b200.plan(batched, n // batched)
+        launches_per_step = len(plan)
+        workload = f"batched: {n // batched} arrays of {batched} random uint32 keys"
+    else:
+        def sort_step():
+            b200.sort_(work)
+        plan = b200.plan(n)
+        launches_per_step = len(plan)
+        workload = f"2^{args.log2n} random uint32 keys, one array, ascending"
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up -------------------------------------------------------------
+    for _ in range(args.warmup):
+        work.copy_(src)
+        sort_step()
+    torch.cuda.synchronize()
+
+    # ---- correctness of the timed configuration (outside timing) -----------
+    if world == 1:
+        ref = src.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        if batched:
+            ref = torch.sort(ref.view(-1, batched), dim=1).values.view(-1)
+        else:
+            ref = torch.sort(ref).values
+        got = work.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        if not torch.equal(got, ref):
+            print(json.dumps({"error": "sort output mismatch"}), flush=True)
+            return 1
+
+    # ---- timed region ----------------------------------------------------------
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sampler = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with sampler:
+        for i in range(args.steps):
+            work.copy_(src)      # restore the unsorted input (not timed)
+            flush.zero_()        # evict L2 (not timed)
+            evs[i][0].record(stream)
+            sort_step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    ms_steps = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(ms_steps) / len(ms_steps)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    keys_total = n * world
+    value = keys_total / (ms * 1e-3) / 1e9
+
+    # ---- per-kernel timing: dominant kernel family -----------------------------
+    roofline = None
+    sort_roof = None
+    if world == 1:
+        fam_t, fam_n, fam_bytes = {}, {}, {}
+        reps = 5
+        for _ in range(reps):
+            work.copy_(src)
+            for i, p in enumerate(plan):
+                flush.zero_() if p.tile_sort else None
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                b200.run_pass_(work, i, n_per_array=(batched or n))
+                e1.record(stream)
+                torch.cuda.synchronize()
+                fam = "tile_sort" if p.tile_sort else "merge"
+                fam_t[fam] = fam_t.get(fam, 0.0) + e0.elapsed_time(e1)
+                fam_n[fam] = fam_n.get(fam, 0) + 1
+        dom = max(fam_t, key=lambda f: fam_t[f])
+        avg_ms = fam_t[dom] / fam_n[dom]
+        alg_bytes = 8 * n  # one read + one write of every key per launch
+        achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": None,
+                    "algorithmic_bytes_per_launch": alg_bytes,
+                    "avg_launch_ms": avg_ms,
+                    "share_of_step": {f: fam_t[f] / sum(fam_t.values()) for f in fam_t}}
+        k = args.log2n if not batched else (batched.bit_length() - 1)
+        pm = 1 if batched else pmin(k)
+        t_roof = pm * 8 * n / (hbm * 1e9)
+        sort_roof = {"p_min": pm, "p_design": len(plan), "t_roof_us": t_roof * 1e6,
+                     "frac": t_roof / (ms * 1e-3),
+                     "definition": "P_min(k,15) x 8 B x n / measured HBM BW (SURVEY 8d)"}
+
+    # ---- end to end through the public API with host buffers ---------------
+    e2e = None
+    if world == 1:
+        h_src = src.cpu().pin_memory()
+        h_out = torch.empty_like(h_src).pin_memory()
+        dwork = torch.empty_like(src)
+        tt = []
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dwork.copy_(h_src, non_blocking=True)
+            if batched:
+                b200.sort_batched_(dwork, batched)
+            else:
+                b200.sort_(dwork)
+            h_out.copy_(dwork, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                tt.append(e0.elapsed_time(e1))
+        ems = sum(tt) / len(tt)
+        e2e = {"value": n / (ems * 1e-3) / 1e9, "unit": "Gkeys/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+               "ms_per_step": ems, "host_buffers": "pinned"}
+
+    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline and not batched:
+        try:
+            kind, cores, c = cpu_baseline(n)
+            qs_gk = n / (c["quicksort_ms"] * 1e-3) / 1e9
+            cpu = {"value": qs_gk, "unit": "Gkeys/s", "cores": 1, "kind": kind,
+                   "sample": f"bitonic::reference_quicksort (the paper's CPU baseline, "
+                             f"verify.cpp:109) on the same 2^{args.log2n} keys, min of reps",
+                   "quicksort_ms": c["quicksort_ms"],
+                   "sequential_bitonic_ms": c["sequential_bitonic_ms"],
+                   "fused_engine_ms": c.get("fused_engine_ms"),
+                   "fused_engine_cores": cores,
+                   "speedup_vs_quicksort": c["quicksort_ms"] / ms,
+                   "speedup_vs_sequential_bitonic": c["sequential_bitonic_ms"] / ms}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic",
+            "config": {"workload": workload, "keys_per_gpu": n, "keys_total": keys_total,
+                       "l2_flush": "256 MiB write before every step (outside timing)",
+                       "input_restore": "D2D copy before every step (outside timing)",
+                       "passes": len(plan)},
+            "e2e": e2e, "roofline": roofline, "sort_roofline": sort_roof,
+            "cpu_baseline": cpu, "clocks": sampler.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "wall_s": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -120,6 +120,14 @@ typedef struct {
 int b200_bitonic_plan(uint64_t n, uint64_t batch, b200_pass_info* out,
                       int max_passes, int* n_passes);
 
+/* Runs only pass `pass_index` of the plan for (n_per_array, batch) on
+ * uint32 keys (profiling aid: running every index in order equals
+ * b200_bitonic_sort_u32_batched).  Returns B200_CONFIG for an index outside
+ * the plan. */
+int b200_bitonic_run_pass_u32(uint32_t* d_keys, uint64_t n_per_array,
+                              uint64_t batch, int descending, int pass_index,
+                              b200_stream_t stream);
+
 /* Counters in the reference's cost model (engine.hpp:55-70, account() in
  * engine.cpp:147-173): {kernel_launches, global_reads, global_writes,
  * compare_exchanges}; reads/writes count keys (x4 for bytes). */

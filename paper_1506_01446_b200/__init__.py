@@ -34,7 +34,7 @@ from . import _native
 
 __all__ = [
     "InvalidSizeError", "ConfigError", "CudaError",
-    "sort_", "sort_batched_", "sequential_bitonic_sort", "sort_host",
+    "sort_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
     "merge_split_", "sort_multi", "plan", "counters", "set_tuning",
     "PassPlan", "version", "library_path",
 ]
@@ -141,6 +141,17 @@ def sequential_bitonic_sort(keys: np.ndarray) -> None:
     if not isinstance(keys, np.ndarray) or keys.dtype != np.int32:
         raise ConfigError("keys must be a numpy int32 array")
     sort_host(keys, descending=False)
+
+
+def run_pass_(t, pass_index: int, n_per_array: Optional[int] = None,
+              descending: bool = False, stream=None):
+    """Run a single pass of the plan on uint32 keys (profiling aid)."""
+    _check_tensor(t)
+    n = n_per_array or t.numel()
+    _check(_native.lib().b200_bitonic_run_pass_u32(
+        ctypes.c_void_p(t.data_ptr()), n, t.numel() // n, int(bool(descending)),
+        int(pass_index), ctypes.c_void_p(_stream_ptr(stream))))
+    return t
 
 
 def merge_split_(local, partner, out, keep_high: bool, key_xor: int = 0,

@@ -23,6 +23,7 @@ EXPORTED = (
     "b200_bitonic_sort_u32_multi",
     "b200_bitonic_merge_split_u32",
     "b200_bitonic_plan",
+    "b200_bitonic_run_pass_u32",
     "b200_bitonic_counters",
     "b200_bitonic_set_tuning",
     "b200_bitonic_last_error",
@@ -70,6 +71,7 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_merge_split_u32.argtypes = [vp, vp, u64, i, ctypes.c_uint32, vp, vp]
     L.b200_bitonic_plan.argtypes = [u64, u64, ctypes.POINTER(PassInfo), i,
                                     ctypes.POINTER(ctypes.c_int)]
+    L.b200_bitonic_run_pass_u32.argtypes = [vp, u64, u64, i, i, vp]
     L.b200_bitonic_counters.argtypes = [u64, u64, ctypes.POINTER(ctypes.c_uint64)]
     L.b200_bitonic_set_tuning.argtypes = [i, i]
     L.b200_bitonic_last_error.restype = ctypes.c_char_p

@@ -137,9 +137,10 @@ cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
                           args, smem, s);
 }
 
-// Validates and runs the whole plan.  key_xor: 0x80000000 for int32 keys.
+// Validates and runs the whole plan (or only pass `only`, when >= 0).
+// key_xor: 0x80000000 for int32 keys.
 int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
-              uint32_t key_xor, cudaStream_t stream) {
+              uint32_t key_xor, cudaStream_t stream, int only = -1) {
   if (n_per < 2 || !is_pow2(n_per)) {
     return fail(B200_INVALID_SIZE,
                 "length must be a power of two >= 2, got " +
@@ -164,7 +165,9 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     return fail(B200_CONFIG, "device pointer must be 16-byte aligned");
   }
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+  if (only >= (int)plan.size()) return fail(B200_CONFIG, "pass index outside the plan");
   for (size_t i = 0; i < plan.size(); ++i) {
+    if (only >= 0 && (int)i != only) continue;
     const b200::PlanPass& q = plan[i];
     b200::PassParams p{};
     p.keys = d_keys;
@@ -460,6 +463,14 @@ int b200_bitonic_plan(uint64_t n, uint64_t batch, b200_pass_info* out,
     out[i].compare_exchanges = q.ces;
   }
   return B200_OK;
+}
+
+int b200_bitonic_run_pass_u32(uint32_t* d_keys, uint64_t n_per_array,
+                              uint64_t batch, int descending, int pass_index,
+                              b200_stream_t stream) {
+  if (pass_index < 0) return fail(B200_CONFIG, "pass index must be >= 0");
+  return sort_impl(d_keys, n_per_array, batch, descending, 0u,
+                   reinterpret_cast<cudaStream_t>(stream), pass_index);
 }
 
 int b200_bitonic_counters(uint64_t n, uint64_t batch, uint64_t out[4]) {
