@@ -206,6 +206,17 @@ struct Tile {
   }
 };
 
+// Programmatic dependent launch: a pass may be launched before the previous
+// pass finished (its launch latency overlaps the previous pass's tail); it
+// waits here until the previous grid's memory is visible.  No-ops when the
+// kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Direction bit (0/1) of global phase p for the key at global index gi.
 __device__ __forceinline__ uint32_t dir_bit_global(uint64_t gi, int p, int kd) {
   return p >= kd ? 0u : (uint32_t)((gi >> p) & 1u);
@@ -219,6 +230,7 @@ bitonic_pass_kernel(PassParams P) {
   constexpr int T = TL::T;
   constexpr int N = TL::N;
   extern __shared__ uint32_t smem[];
+  pdl_wait();
 
   // ---- global base of this CTA's coset ----------------------------------
   const int a = P.a, y = P.y, h = C - a;
@@ -376,6 +388,7 @@ bitonic_pass_kernel(PassParams P) {
       P.keys[gidx(j)] = smem[TL::pad(j)] ^ m;
     }
   }
+  pdl_trigger();
 }
 
 }  // namespace b200

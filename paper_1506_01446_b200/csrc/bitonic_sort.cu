@@ -95,6 +95,7 @@ b200::PassFn generic_kernel(int C) {
 }
 
 std::atomic<int> g_force_generic{0};
+std::atomic<int> g_pdl{1};  // programmatic dependent launch between passes
 
 b200::PassFn select_kernel(const b200::PlanPass& q) {
   if (!g_force_generic.load()) {
@@ -133,8 +134,17 @@ cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
   if (e != cudaSuccess) return e;
   const size_t smem = (size_t)b200::tile_smem_words(q.C) * 4;
   void* args[] = {&p};
-  return cudaLaunchKernel(fn, dim3((unsigned)q.ctas), dim3(b200::tile_threads(q.C)),
-                          args, smem, s);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)q.ctas);
+  cfg.blockDim = dim3(b200::tile_threads(q.C));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl.load() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 // Validates and runs the whole plan (or only pass `only`, when >= 0).
@@ -491,6 +501,9 @@ int b200_bitonic_counters(uint64_t n, uint64_t batch, uint64_t out[4]) {
 int b200_bitonic_set_tuning(int tile_bits, int min_run_bits) {
   // min_run_bits >= 100 selects the runtime-dispatched kernels (testing aid):
   // b200_bitonic_set_tuning(t, 100 + r) == (t, r) with generic kernels.
+  // min_run_bits >= 1000 disables programmatic dependent launch (testing aid)
+  g_pdl.store(min_run_bits >= 1000 ? 0 : 1);
+  if (min_run_bits >= 1000) min_run_bits -= 1000;
   g_force_generic.store(min_run_bits >= 100 ? 1 : 0);
   if (min_run_bits >= 100) min_run_bits -= 100;
   if (tile_bits != 0 && (tile_bits < 6 || tile_bits > b200::kMaxTileBits)) {

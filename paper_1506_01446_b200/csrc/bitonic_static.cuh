@@ -261,9 +261,11 @@ struct PassBody {
 
   __device__ __forceinline__ static void run(const Ctx& c, uint32_t* sm) {
     uint32_t v[NR];
+    pdl_wait();
     load(c, sm, v);
     rounds<0>(c, sm, v);
     store(c, sm, v);
+    pdl_trigger();
   }
 };
 
