@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb200_bitonic.so")
+# B200_BITONIC_LIB overrides the library path (A/B performance experiments).
+LIB_PATH = os.environ.get("B200_BITONIC_LIB") or os.path.join(HERE, "libb200_bitonic.so")
 
 # Every symbol include/b200_bitonic.h declares (tests check the .so exports
 # exactly these).

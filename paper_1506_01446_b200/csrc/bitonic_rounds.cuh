@@ -91,7 +91,7 @@ constexpr bool lanes_feasible(uint32_t m) {
 // ends early when its register set would make a conflict-free lane choice
 // impossible (only enforced for C >= 10, where every residue has two
 // positions).
-template <class S, int C, int R>
+template <class S, int C, int R, int A = C>
 struct Rounds {
   static constexpr bool enforce = C >= 10 && C - R >= 5;
   static constexpr int next_begin(int b) {
@@ -119,12 +119,19 @@ struct Rounds {
     }
     return r;
   }
-  // Register set of round r: its step bits, padded to R bits with the
-  // highest unused bits (keeps the lanes on the low bits).
+  // Register set of round r: its step bits, padded to R bits.  Fillers come
+  // first from [5, A) -- above the lanes but inside the coset's contiguous
+  // run, so direct HBM access needs fewer per-register pointers -- then from
+  // the top (keeps the lanes on the low bits).
   static constexpr uint32_t mask(int r) {
     uint32_t m = 0;
     const int e = begin(r + 1);
     for (int i = begin(r); i < e; ++i) m |= 1u << S::bit(i);
+    for (int b = A - 1; b >= 5 && popc(m) < R; --b) {
+      if (m & (1u << b)) continue;
+      if (enforce && !lanes_feasible<C>(m | (1u << b))) continue;
+      m |= 1u << b;
+    }
     for (int b = C - 1; b >= 0 && popc(m) < R; --b) {
       if (m & (1u << b)) continue;
       if (enforce && !lanes_feasible<C>(m | (1u << b))) continue;
@@ -174,9 +181,34 @@ struct Layout {
       if (lane_pos(r) == p) return true;
     return false;
   }
-  // position of thread bit i: lanes first (one per residue), then the
-  // remaining free positions ascending
+  // number of consecutive register bits starting at bit 0
+  static constexpr int vec_bits() {
+    int v = 0;
+    while (v < C && (RM & (1u << v))) ++v;
+    return v;
+  }
+  // lanes on the 5 bits just above the low register run: a warp then owns
+  // 32 x 2^v consecutive keys (coalesced vector access, v <= 2)
+  static constexpr bool contiguous_lanes() {
+    const int v = vec_bits();
+    if (C - R < 5 || v > 2 || v + 5 > C) return false;
+    for (int b = v; b < v + 5; ++b)
+      if (RM & (1u << b)) return false;
+    return true;
+  }
+  // position of thread bit i: lanes first (5 contiguous bits when possible,
+  // else one per residue), then the remaining free positions ascending
   static constexpr int tpos(int i) {
+    if (contiguous_lanes()) {
+      const int v = vec_bits();
+      if (i < 5) return v + i;
+      int k = 4;
+      for (int b = 0; b < C; ++b)
+        if (!(RM & (1u << b)) && !(b >= v && b < v + 5)) {
+          if (++k == i) return b;
+        }
+      return -1;
+    }
     if (!residue_lanes()) return free_pos(i);
     if (i < 5) return lane_pos(i);
     int k = 4;
@@ -216,11 +248,8 @@ struct Layout {
     return true;
   }
   static_assert(C < 10 || conflict_free(), "shared-memory layout has bank conflicts");
-  // lanes own consecutive keys (direct coalesced global access)
-  static constexpr bool lanes_low() {
-    return (RM & 31u) == 0 && C - R >= 5 && tpos(0) == 0 && tpos(1) == 1 &&
-           tpos(2) == 2 && tpos(3) == 3 && tpos(4) == 4;
-  }
+  // lanes own consecutive 2^v-key vectors (direct coalesced global access)
+  static constexpr bool lanes_low() { return contiguous_lanes(); }
 
   // length of the run of consecutive thread bits starting at thread bit i
   // that land on consecutive local bits

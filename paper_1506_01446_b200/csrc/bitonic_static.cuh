@@ -18,6 +18,43 @@
 
 namespace b200 {
 
+// ---- global access primitives ---------------------------------------------------
+// Inline PTX keeps the 32 per-register accesses in register order (volatile
+// asm is not reordered), which keeps the DRAM access order of all CTAs alike;
+// B200_LDG_OP / B200_STG_OP select the cache operator (experiments).
+#ifndef B200_LDG_OP
+#define B200_LDG_OP ".lu"  // last use: measured best for the streaming passes
+#endif
+#ifndef B200_STG_OP
+#define B200_STG_OP ""
+#endif
+__device__ __forceinline__ uint32_t ldg32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global" B200_LDG_OP ".u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ldg64(const uint32_t* p) {
+  uint2 v;
+  asm volatile("ld.global" B200_LDG_OP ".v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint4 ldg128(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.global" B200_LDG_OP ".v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg32(uint32_t* p, uint32_t v) {
+  asm volatile("st.global" B200_STG_OP ".u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void stg64(uint32_t* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global" B200_STG_OP ".v2.u32 [%0], {%1, %2};" :: "l"(p), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void stg128(uint32_t* p, uint4 v) {
+  asm volatile("st.global" B200_STG_OP ".v4.u32 [%0], {%1, %2, %3, %4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
 // ---- coset geometry ----------------------------------------------------------
 template <int C, int A>
 struct Coset {
@@ -42,6 +79,10 @@ struct Coset {
 };
 
 // ---- staging (coalesced HBM <-> padded shared memory) ------------------------
+// Thread t moves the uint4 at local index j = 4t + it*4T for it = 0..IT-1.
+// The two terms occupy disjoint local bits, so the global offset is
+// goff(4t) + goff(it*4T): one per-thread base plus a uniform per-iteration
+// offset (no per-key index arithmetic).
 template <int C, int A, int DBIT>
 __device__ __forceinline__ void stage_in(uint32_t* sm, const uint32_t* keys,
                                          uint64_t gbase, int y, uint32_t m_uniform) {
@@ -49,15 +90,16 @@ __device__ __forceinline__ void stage_in(uint32_t* sm, const uint32_t* keys,
   constexpr int T = TL::T, N = TL::N;
   if constexpr (N / T >= 4) {
     constexpr int IT = N / 4 / T;
+    const uint32_t j0 = 4u * threadIdx.x;
+    const uint32_t* base = keys + gbase + Coset<C, A>::goff(j0, y);
     uint4 buf[IT];
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const uint32_t j = 4u * (uint32_t)(it * T + threadIdx.x);
-      buf[it] = *reinterpret_cast<const uint4*>(keys + gbase + Coset<C, A>::goff(j, y));
+      buf[it] = ldg128(base + Coset<C, A>::goff((uint32_t)(it * 4 * T), y));
     }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const uint32_t j = 4u * (uint32_t)(it * T + threadIdx.x);
+      const uint32_t j = j0 + (uint32_t)(it * 4 * T);
       uint32_t m = m_uniform;
       if constexpr (DBIT >= 0) m ^= 0u - ((j >> DBIT) & 1u);
       const uint32_t pj = TL::pad(j);
@@ -84,16 +126,17 @@ __device__ __forceinline__ void stage_out(const uint32_t* sm, uint32_t* keys,
   __syncthreads();
   if constexpr (N / T >= 4) {
     constexpr int IT = N / 4 / T;
+    const uint32_t j0 = 4u * threadIdx.x;
+    uint32_t* base = keys + gbase + Coset<C, A>::goff(j0, y);
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const uint32_t j = 4u * (uint32_t)(it * T + threadIdx.x);
-      const uint32_t pj = TL::pad(j);
+      const uint32_t pj = TL::pad(j0 + (uint32_t)(it * 4 * T));
       uint4 q;
       q.x = sm[pj + 0];
       q.y = sm[pj + 1];
       q.z = sm[pj + 2];
       q.w = sm[pj + 3];
-      *reinterpret_cast<uint4*>(keys + gbase + Coset<C, A>::goff(j, y)) = q;
+      stg128(base + Coset<C, A>::goff((uint32_t)(it * 4 * T), y), q);
     }
   } else {
     for (uint32_t j = threadIdx.x; j < (uint32_t)N; j += T) {
@@ -120,9 +163,9 @@ struct PassBody {
   using S = Seq<C, KIND, SA, SB>;
   static constexpr int R = reg_bits(C);
   static constexpr int NR = 1 << R;
-  using RD = Rounds<S, C, R>;
-  static constexpr int NRND = RD::count();
   static constexpr int A = KIND == 0 ? C : (SB >= 0 ? SB : C);
+  using RD = Rounds<S, C, R, A>;
+  static constexpr int NRND = RD::count();
   template <int r>
   using L = Layout<C, RD::mask(r)>;
 
@@ -206,17 +249,66 @@ struct PassBody {
     }
   }
 
+  // Direct (coalesced) HBM access is possible for a round's layout when its
+  // lanes sit on 5 contiguous bits v..v+4 above a low register run of v <= 2
+  // bits, all inside the contiguous low run of the coset (A >= v + 5).
+  template <class LR>
+  static constexpr bool direct_ok() {
+    return KIND == 1 && LR::lanes_low() && A >= LR::vec_bits() + 5;
+  }
+  template <class LR>
+  __device__ __forceinline__ static void gload(const Ctx& c, uint32_t tj, uint32_t (&v)[NR]) {
+    constexpr int V = LR::vec_bits();
+    const uint32_t* base = c.keys + c.gbase + Coset<C, A>::goff(tj, c.y);
+    if constexpr (V == 0) {
+#pragma unroll
+      for (int e = 0; e < NR; ++e) v[e] = ldg32(base + Coset<C, A>::goff(LR::dep_reg(e), c.y));
+    } else if constexpr (V == 1) {
+#pragma unroll
+      for (int e = 0; e < NR; e += 2) {
+        const uint2 q = ldg64(base + Coset<C, A>::goff(LR::dep_reg(e), c.y));
+        v[e] = q.x;
+        v[e + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NR; e += 4) {
+        const uint4 q = ldg128(base + Coset<C, A>::goff(LR::dep_reg(e), c.y));
+        v[e] = q.x;
+        v[e + 1] = q.y;
+        v[e + 2] = q.z;
+        v[e + 3] = q.w;
+      }
+    }
+  }
+  template <class LR>
+  __device__ __forceinline__ static void gstore(const Ctx& c, uint32_t tj, const uint32_t (&v)[NR]) {
+    constexpr int V = LR::vec_bits();
+    uint32_t* base = c.keys + c.gbase + Coset<C, A>::goff(tj, c.y);
+    if constexpr (V == 0) {
+#pragma unroll
+      for (int e = 0; e < NR; ++e) stg32(base + Coset<C, A>::goff(LR::dep_reg(e), c.y), v[e]);
+    } else if constexpr (V == 1) {
+#pragma unroll
+      for (int e = 0; e < NR; e += 2) {
+        stg64(base + Coset<C, A>::goff(LR::dep_reg(e), c.y), v[e], v[e + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NR; e += 4) {
+        stg128(base + Coset<C, A>::goff(LR::dep_reg(e), c.y),
+               make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+      }
+    }
+  }
+
   // Keys -> registers in round 0's layout (phase domain of the first step).
   __device__ __forceinline__ static void load(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR]) {
     using L0 = L<0>;
     constexpr int PH = S::phase(0);
-    if constexpr (KIND == 1 && L0::lanes_low() && A >= 5) {
+    if constexpr (direct_ok<L0>()) {
       const uint32_t tj = L0::thread_j();
-      const uint32_t* base = c.keys + c.gbase + Coset<C, A>::goff(tj, c.y);
-#pragma unroll
-      for (int e = 0; e < NR; ++e) {
-        v[e] = base[Coset<C, A>::goff(L0::dep_reg(e), c.y)];
-      }
+      gload<L0>(c, tj, v);
 #pragma unroll
       for (int e = 0; e < NR; ++e) v[e] ^= dmask<L0, PH>(c, e, tj) ^ c.gin;
     } else {
@@ -234,12 +326,8 @@ struct PassBody {
     const uint32_t tj = LL::thread_j();
 #pragma unroll
     for (int e = 0; e < NR; ++e) v[e] ^= dmask<LL, PH>(c, e, tj) ^ c.gout;
-    if constexpr (KIND == 1 && LL::lanes_low() && A >= 5) {
-      uint32_t* base = c.keys + c.gbase + Coset<C, A>::goff(tj, c.y);
-#pragma unroll
-      for (int e = 0; e < NR; ++e) {
-        base[Coset<C, A>::goff(LL::dep_reg(e), c.y)] = v[e];
-      }
+    if constexpr (direct_ok<LL>()) {
+      gstore<LL>(c, tj, v);
     } else {
       LL::sts(sm, v);
       stage_out<C, A>(sm, c.keys, c.gbase, c.y);
@@ -299,7 +387,7 @@ merge_kernel(PassParams P) {
   c.uA = 0u - dir_bit_global(c.gbase, P.pA, P.kd);
   c.uB = 0u - dir_bit_global(c.gbase, P.pB, P.kd);
   c.uC = 0u;
-  c.gin = P.gmask_in;
+  c.gin = 0u;  // a merge pass never runs first: keys are already transformed
   c.gout = P.gmask_out;
   B::run(c, smem);
 }

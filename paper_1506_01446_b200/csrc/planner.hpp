@@ -37,10 +37,10 @@ struct PlanPass {
 };
 
 struct PlanOptions {
-  int cmax = 14;   // largest tile (2^cmax keys per CTA)
+  int cmax = 15;   // largest tile (2^cmax keys per CTA)
   int lrun = 5;    // min contiguous run per merge pass (2^lrun keys)
   int min_ctas = 128;  // shrink the tile until the grid has this many CTAs
-  int cmin = 10;   // ... but not below this tile size
+  int cmin = 6;    // ... but not below this tile size
 };
 
 inline int ctz64(uint64_t x) {
@@ -62,21 +62,33 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   const int kt = k + ctz64(batch);  // tiles must divide the whole buffer
   std::vector<PlanPass> plan;
 
-  // Tile size: as large as allowed, shrunk for small problems so the grid
-  // still covers the SMs.
-  int C = opt.cmax;
-  if (k <= 15 && k > C) C = k;  // one array fits one CTA: a single launch
-  // Batched arrays of >= 2^8 keys: one array per CTA (the specialised tile
-  // sort runs exactly phases 1..C).  Smaller arrays share a tile.
-  if (batch > 1 && k >= 8 && k <= 15) C = k;
-  if (C > kt) C = kt;
-  // Shrink the tile for small problems so the grid still covers the SMs --
-  // but never below k when the whole array fits one tile (that would add
-  // merge passes).
-  while (C > opt.cmin && C > k && (total >> C) < (uint64_t)opt.min_ctas) --C;
-  if (k > C) {
-    while (C > opt.cmin && (total >> C) < (uint64_t)opt.min_ctas) --C;
+  // Tile size.  With an explicit tuning (cmin == cmax) use it; otherwise the
+  // per-size choice measured best on B200 (PDL between passes):
+  //   k <= 12  one CTA sorts the whole array (single launch)
+  //   13..18   2^12-key tiles (latency-bound: spread over more SMs)
+  //   19..25   2^13-key tiles (128+ CTAs, L2-resident passes at 2^20)
+  //   >= 26    2^14-key tiles (HBM-bound: fewer passes)
+  int C;
+  if (opt.cmin == opt.cmax) {
+    C = opt.cmax;
+  } else if (k <= 12) {
+    C = k;
+  } else if (k <= 18) {
+    C = 12;
+  } else if (k <= 25) {
+    C = 13;
+  } else {
+    C = 14;
   }
+  if (C > opt.cmax) C = opt.cmax > k ? k : opt.cmax;
+  if (batch > 1) {
+    // Batched arrays of >= 2^8 keys: one array per CTA (the specialised
+    // tile sort runs exactly phases 1..C); smaller arrays share a tile.
+    if (k >= 8 && k <= 15) C = k;
+    else if (k < 8) C = opt.cmax;
+    while (C > k && C > opt.cmin && (total >> C) < (uint64_t)opt.min_ctas) --C;
+  }
+  if (C > kt) C = kt;
   // Merge passes need a coalescing run below the high range and a phase
   // direction bit that is per-thread uniform in layout L_0 (C - 1 >= 5).
   if (k > C && C < opt.lrun + 1) C = opt.lrun + 1;
