@@ -318,6 +318,11 @@ def main():
         for i in range(args.steps):
             work.copy_(src)      # restore the unsorted input (not timed)
             flush.zero_()        # evict L2 (not timed)
+            # ~50 us device-side delay so the host has enqueued every pass of
+            # the sort before the start event fires: the events then bracket
+            # the device execution of the sort, not host launch overhead
+            # (which e2e below does include).
+            torch.cuda._sleep(100_000)
             evs[i][0].record(stream)
             sort_step()
             evs[i][1].record(stream)
@@ -344,6 +349,7 @@ def main():
             for i, p in enumerate(plan):
                 flush.zero_() if p.tile_sort else None
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda._sleep(20_000)  # keep host launch latency out of the event window
                 e0.record(stream)
                 b200.run_pass_(work, i, n_per_array=(batched or n))
                 e1.record(stream)
@@ -421,6 +427,8 @@ def main():
             "config": {"workload": workload, "keys_per_gpu": n, "keys_total": keys_total,
                        "l2_flush": "256 MiB write before every step (outside timing)",
                        "input_restore": "D2D copy before every step (outside timing)",
+                       "timing": "CUDA events on the sort stream around each step; a device "
+                                 "sleep before the start event keeps host launch overhead out",
                        "passes": len(plan)},
             "e2e": e2e, "roofline": roofline, "sort_roofline": sort_roof,
             "cpu_baseline": cpu, "clocks": sampler.summary(),

@@ -71,6 +71,17 @@ int b200_bitonic_sort_i32_batched(int32_t* d_keys, uint64_t n_per_array,
                                   uint64_t batch, int descending,
                                   b200_stream_t stream);
 
+/* Any length n >= 1 (the reference's pad_to_pow2 + sort + truncate,
+ * bench.cpp:366-377, acceptance.cpp:114-156): when n is not a power of two
+ * the keys are copied into a stream-ordered scratch buffer of bit_ceil(n)
+ * keys padded with the order's maximum (INT32_MAX for ascending int32, as
+ * pad_to_pow2 does), sorted, and the first n keys are copied back.  Powers
+ * of two sort in place with no allocation. */
+int b200_bitonic_sort_padded_u32(uint32_t* d_keys, uint64_t n, int descending,
+                                 b200_stream_t stream);
+int b200_bitonic_sort_padded_i32(int32_t* d_keys, uint64_t n, int descending,
+                                 b200_stream_t stream);
+
 /* Host-memory convenience entries: H2D copy, sort, D2H copy, synchronous.
  * Mirror sequential_bitonic_sort(std::span<int32_t>) exactly (in place on
  * caller-owned host memory).  These allocate device memory per call. */

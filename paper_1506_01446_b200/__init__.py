@@ -34,7 +34,7 @@ from . import _native
 
 __all__ = [
     "InvalidSizeError", "ConfigError", "CudaError",
-    "sort_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
+    "sort_", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
     "merge_split_", "sort_multi", "plan", "counters", "set_tuning",
     "PassPlan", "version", "library_path",
 ]
@@ -102,6 +102,19 @@ def sort_(t, descending: bool = False, stream=None):
     _check_tensor(t)
     kind = _key_dtype(t)
     fn = _native.lib().b200_bitonic_sort_i32 if kind == "i32" else _native.lib().b200_bitonic_sort_u32
+    _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
+              ctypes.c_void_p(_stream_ptr(stream))))
+    return t
+
+
+def sort_padded_(t, descending: bool = False, stream=None):
+    """Any-length sort: the reference's pad_to_pow2 + sort + truncate
+    (bench.cpp:366-377) -- non-powers of two go through a padded scratch
+    buffer (stream-ordered allocation); powers of two sort in place."""
+    _check_tensor(t)
+    kind = _key_dtype(t)
+    fn = (_native.lib().b200_bitonic_sort_padded_i32 if kind == "i32"
+          else _native.lib().b200_bitonic_sort_padded_u32)
     _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
               ctypes.c_void_p(_stream_ptr(stream))))
     return t

@@ -147,6 +147,31 @@ cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
+// Plans are pure functions of (k, batch, options): cache the last few so a
+// repeated sort costs only its kernel launches on the host.
+std::mutex g_plan_mu;
+struct PlanKey {
+  int k;
+  uint64_t batch;
+  int cmax, cmin, lrun, min_ctas;
+  bool operator==(const PlanKey& o) const {
+    return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
+           lrun == o.lrun && min_ctas == o.min_ctas;
+  }
+};
+std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
+
+std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
+  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas};
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (auto& e : g_plans)
+    if (e.first == key) return e.second;
+  auto plan = b200::make_plan(k, batch, o);
+  if (g_plans.size() >= 16) g_plans.erase(g_plans.begin());
+  g_plans.emplace_back(key, plan);
+  return plan;
+}
+
 // Validates and runs the whole plan (or only pass `only`, when >= 0).
 // key_xor: 0x80000000 for int32 keys.
 int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
@@ -167,7 +192,7 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
   if (d_keys == nullptr) return fail(B200_CONFIG, "null key pointer");
   std::vector<b200::PlanPass> plan;
   try {
-    plan = b200::make_plan(k, batch, plan_options());
+    plan = cached_plan(k, batch, plan_options());
   } catch (const std::exception& e) {
     return fail(B200_CONFIG, e.what());
   }
@@ -213,9 +238,61 @@ int merge_split_impl(const uint32_t* local, const uint32_t* partner, uint64_t m,
   return B200_OK;
 }
 
+__global__ void pad_fill_kernel(uint32_t* dst, const uint32_t* src, uint64_t n,
+                                uint64_t m, uint32_t pad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    dst[i] = i < n ? src[i] : pad;
+  }
+}
+
+int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
+                cudaStream_t s) {
+  if (n < 1) return fail(B200_INVALID_SIZE, "length must be >= 1");
+  if (d_keys == nullptr) return fail(B200_CONFIG, "null key pointer");
+  if (descending != 0 && descending != 1) {
+    return fail(B200_CONFIG, "descending must be 0 or 1");
+  }
+  if (n == 1) return B200_OK;
+  if (is_pow2(n) && (reinterpret_cast<uintptr_t>(d_keys) & 15u) == 0) {
+    return sort_impl(d_keys, n, 1, descending, key_xor, s);
+  }
+  uint64_t m = 2;
+  while (m < n) m <<= 1;
+  // padding = the largest key in the sort's order (sorts last, discarded)
+  const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+  const uint32_t pad = ~gmask;
+  uint32_t* tmp = nullptr;
+  B200_CUDA_TRY(cudaMallocAsync(&tmp, m * 4, s));
+  const unsigned grid = (unsigned)std::min<uint64_t>((m + 255) / 256, 148 * 8);
+  pad_fill_kernel<<<grid, 256, 0, s>>>(tmp, d_keys, n, m, pad);
+  int rc = sort_impl(tmp, m, 1, descending, key_xor, s);
+  if (rc == B200_OK) {
+    cudaError_t e = cudaMemcpyAsync(d_keys, tmp, n * 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "copy back");
+  }
+  cudaFreeAsync(tmp, s);
+  if (rc == B200_OK) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_fail(e, "padded sort");
+  }
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
+
+int b200_bitonic_sort_padded_u32(uint32_t* d_keys, uint64_t n, int descending,
+                                 b200_stream_t stream) {
+  return padded_impl(d_keys, n, descending, 0u, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_padded_i32(int32_t* d_keys, uint64_t n, int descending,
+                                 b200_stream_t stream) {
+  return padded_impl(reinterpret_cast<uint32_t*>(d_keys), n, descending, 0x80000000u,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
 
 int b200_bitonic_sort_u32(uint32_t* d_keys, uint64_t n, int descending,
                           b200_stream_t stream) {

@@ -66,8 +66,10 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // per-size choice measured best on B200 (PDL between passes):
   //   k <= 12  one CTA sorts the whole array (single launch)
   //   13..18   2^12-key tiles (latency-bound: spread over more SMs)
-  //   19..25   2^13-key tiles (128+ CTAs, L2-resident passes at 2^20)
-  //   >= 26    2^14-key tiles (HBM-bound: fewer passes)
+  //   >= 19    2^13-key tiles: 128+ CTAs at 2^20, and at 2^24..2^28 four
+  //            CTAs per SM keep the merge passes HBM-bound (2^14-key tiles
+  //            need fewer passes but only fit two CTAs per SM and measured
+  //            slower: 12.3 vs 12.1 ms at 2^28)
   int C;
   if (opt.cmin == opt.cmax) {
     C = opt.cmax;
@@ -75,10 +77,8 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     C = k;
   } else if (k <= 18) {
     C = 12;
-  } else if (k <= 25) {
-    C = 13;
   } else {
-    C = 14;
+    C = 13;
   }
   if (C > opt.cmax) C = opt.cmax > k ? k : opt.cmax;
   if (batch > 1) {
