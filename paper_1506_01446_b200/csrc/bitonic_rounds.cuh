@@ -248,6 +248,14 @@ struct Layout {
     return true;
   }
   static_assert(C < 10 || conflict_free(), "shared-memory layout has bank conflicts");
+  // local bit b is a warp bit (a thread bit that is not one of the 5 lanes)
+  static constexpr bool is_warp_bit(int b) {
+    if (RM & (1u << b)) return false;
+    const int lanes = (C - R) < 5 ? (C - R) : 5;
+    for (int i = 0; i < lanes; ++i)
+      if (tpos(i) == b) return false;
+    return true;
+  }
   // lanes own consecutive 2^v-key vectors (direct coalesced global access)
   static constexpr bool lanes_low() { return contiguous_lanes(); }
 

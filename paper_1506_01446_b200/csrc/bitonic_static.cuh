@@ -193,6 +193,90 @@ struct PassBody {
     return ph == 0 ? c.uA : c.uB;
   }
 
+  // Direction source of phase id PH in layout LR:
+  //   register bit (compile-time per register), thread bit (runtime, maybe
+  //   warp-uniform), CTA-uniform value, or none (natural domain).
+  template <class LR, int PH>
+  static constexpr int reg_q() {
+    if (natural(PH)) return -1;
+    constexpr int lb = dloc(PH);
+    if (lb < 0) return -1;
+    return LR::qof(lb);
+  }
+  template <class LR, int PH>
+  static constexpr bool warp_uniform() {
+    if (natural(PH)) return true;
+    constexpr int lb = dloc(PH);
+    if (lb < 0) return true;            // CTA-uniform
+    if (LR::qof(lb) >= 0) return true;  // register part: no runtime value
+    return LR::is_warp_bit(lb);
+  }
+  // runtime (non-register) part of phase PH's mask for this thread: 0 / ~0
+  template <class LR, int PH>
+  __device__ __forceinline__ static uint32_t uni_part(const Ctx& c, uint32_t tj) {
+    if constexpr (natural(PH)) {
+      return 0u;
+    } else {
+      constexpr int lb = dloc(PH);
+      if constexpr (lb < 0) {
+        return uni(c, PH);
+      } else if constexpr (LR::qof(lb) >= 0) {
+        return 0u;
+      } else {
+        return 0u - ((tj >> lb) & 1u);
+      }
+    }
+  }
+
+  // XOR register e with D_PH0(e) ^ D_PH1(e) ^ extra (PH < 0: no phase).
+  // When the runtime part is warp-uniform the branch is divergence-free and
+  // only the registers that actually flip are complemented.
+  template <class LR, int PH0, int PH1, bool EXTRA_WARP_UNIFORM>
+  __device__ __forceinline__ static void apply_mask(const Ctx& c, uint32_t (&v)[NR],
+                                                    uint32_t extra) {
+    constexpr int q0 = PH0 >= 0 ? reg_q<LR, PH0>() : -1;
+    constexpr int q1 = PH1 >= 0 ? reg_q<LR, PH1>() : -1;
+    // (measured: helps the ALU-bound tile sort, hurts the latency-bound
+    // merge passes at 2^20 -- so merges keep the straight XOR)
+    constexpr bool wu = KIND == 0 && EXTRA_WARP_UNIFORM && (PH0 < 0 || warp_uniform<LR, PH0>()) &&
+                        (PH1 < 0 || warp_uniform<LR, PH1>());
+    const uint32_t tj = LR::thread_j();
+    uint32_t u = 0u;  // runtime direction part: 0 or ~0
+    if constexpr (PH0 >= 0) u ^= uni_part<LR, PH0>(c, tj);
+    if constexpr (PH1 >= 0) u ^= uni_part<LR, PH1>(c, tj);
+    auto rbit = [](int e) -> bool {
+      bool r = false;
+      if (q0 >= 0) r ^= ((e >> q0) & 1) != 0;
+      if (q1 >= 0) r ^= ((e >> q1) & 1) != 0;
+      return r;
+    };
+    if constexpr (wu) {
+      if (u) {
+#pragma unroll
+        for (int e = 0; e < NR; ++e)
+          if (!rbit(e)) v[e] = ~v[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < NR; ++e)
+          if (rbit(e)) v[e] = ~v[e];
+      }
+      // key-order transform (arbitrary CTA-uniform constant, usually 0)
+      if (extra) {
+#pragma unroll
+        for (int e = 0; e < NR; ++e) v[e] ^= extra;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NR; ++e) v[e] ^= (rbit(e) ? ~u : u) ^ extra;
+    }
+  }
+
+  template <class LR, int PH0, int PH1>
+  __device__ __forceinline__ static void transition(const Ctx& c, uint32_t (&v)[NR],
+                                                    uint32_t extra) {
+    apply_mask<LR, PH0, PH1, true>(c, v, extra);
+  }
+
   // Mask of register e, layout LR, phase id ph (0 / ~0).
   template <class LR, int PH>
   __device__ __forceinline__ static uint32_t dmask(const Ctx& c, int e, uint32_t tj) {
@@ -209,17 +293,6 @@ struct PassBody {
       } else {
         return uni(c, PH);
       }
-    }
-  }
-
-  template <class LR, int PH0, int PH1>
-  __device__ __forceinline__ static void transition(const Ctx& c, uint32_t (&v)[NR],
-                                                    uint32_t extra) {
-    const uint32_t tj = LR::thread_j();
-#pragma unroll
-    for (int e = 0; e < NR; ++e) {
-      const uint32_t m = dmask<LR, PH0>(c, e, tj) ^ dmask<LR, PH1>(c, e, tj) ^ extra;
-      v[e] ^= m;
     }
   }
 
@@ -309,8 +382,7 @@ struct PassBody {
     if constexpr (direct_ok<L0>()) {
       const uint32_t tj = L0::thread_j();
       gload<L0>(c, tj, v);
-#pragma unroll
-      for (int e = 0; e < NR; ++e) v[e] ^= dmask<L0, PH>(c, e, tj) ^ c.gin;
+      apply_mask<L0, PH, -1, true>(c, v, c.gin);
     } else {
       constexpr int db = natural(PH) ? -1 : dloc(PH);
       const uint32_t u = (natural(PH) || db >= 0) ? 0u : uni(c, PH);
@@ -324,8 +396,7 @@ struct PassBody {
     using LL = L<NRND - 1>;
     constexpr int PH = S::phase(S::len() - 1);
     const uint32_t tj = LL::thread_j();
-#pragma unroll
-    for (int e = 0; e < NR; ++e) v[e] ^= dmask<LL, PH>(c, e, tj) ^ c.gout;
+    apply_mask<LL, PH, -1, true>(c, v, c.gout);
     if constexpr (direct_ok<LL>()) {
       gstore<LL>(c, tj, v);
     } else {
