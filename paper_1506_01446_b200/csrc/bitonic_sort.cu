@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -54,6 +55,7 @@ b200::PlanOptions plan_options() {
     o.cmin = tb;  // explicit tile size: no automatic shrinking
   }
   o.lrun = g_min_run_bits.load();
+  if (const char* e = std::getenv("B200_BITONIC_REGBITS")) o.regbits = std::atoi(e);
   return o;
 }
 
@@ -97,13 +99,22 @@ b200::PassFn generic_kernel(int C) {
 std::atomic<int> g_force_generic{0};
 std::atomic<int> g_pdl{1};  // programmatic dependent launch between passes
 
-b200::PassFn select_kernel(const b200::PlanPass& q) {
+// Returns the kernel and its keys-per-thread exponent (the block size is
+// 2^(C - R)).  Shapes without a 16-keys-per-thread instantiation fall back to
+// 32 keys per thread.
+b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out) {
   if (!g_force_generic.load()) {
-    b200::PassFn f = q.tile_sort
-                         ? (q.p_end == q.C ? b200::find_tile_kernel(q.C) : nullptr)
-                         : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo);
-    if (f) return f;
+    for (int R : {q.R, 5}) {
+      b200::PassFn f = q.tile_sort
+                           ? (q.p_end == q.C ? b200::find_tile_kernel(q.C, R) : nullptr)
+                           : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo, R);
+      if (f) {
+        *R_out = R == 5 ? b200::reg_bits(q.C) : R;
+        return f;
+      }
+    }
   }
+  *R_out = b200::reg_bits(q.C);
   return generic_kernel(q.C);
 }
 
@@ -128,7 +139,8 @@ cudaError_t ensure_attr(const void* fn, int C) {
 
 cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
                         cudaStream_t s) {
-  b200::PassFn f = select_kernel(q);
+  int R = 5;
+  b200::PassFn f = select_kernel(q, &R);
   const void* fn = reinterpret_cast<const void*>(f);
   cudaError_t e = ensure_attr(fn, q.C);
   if (e != cudaSuccess) return e;
@@ -136,7 +148,7 @@ cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
   void* args[] = {&p};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)q.ctas);
-  cfg.blockDim = dim3(b200::tile_threads(q.C));
+  cfg.blockDim = dim3(1u << (q.C - R));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -153,16 +165,16 @@ std::mutex g_plan_mu;
 struct PlanKey {
   int k;
   uint64_t batch;
-  int cmax, cmin, lrun, min_ctas;
+  int cmax, cmin, lrun, min_ctas, regbits;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
-           lrun == o.lrun && min_ctas == o.min_ctas;
+           lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
-  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas};
+  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;

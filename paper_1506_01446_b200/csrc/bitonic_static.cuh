@@ -83,11 +83,11 @@ struct Coset {
 // The two terms occupy disjoint local bits, so the global offset is
 // goff(4t) + goff(it*4T): one per-thread base plus a uniform per-iteration
 // offset (no per-key index arithmetic).
-template <int C, int A, int DBIT>
+template <int C, int A, int DBIT, int R>
 __device__ __forceinline__ void stage_in(uint32_t* sm, const uint32_t* keys,
                                          uint64_t gbase, int y, uint32_t m_uniform) {
   using TL = Tile<C>;
-  constexpr int T = TL::T, N = TL::N;
+  constexpr int T = 1 << (C - R), N = TL::N;
   if constexpr (N / T >= 4) {
     constexpr int IT = N / 4 / T;
     const uint32_t j0 = 4u * threadIdx.x;
@@ -118,11 +118,11 @@ __device__ __forceinline__ void stage_in(uint32_t* sm, const uint32_t* keys,
   __syncthreads();
 }
 
-template <int C, int A>
+template <int C, int A, int R>
 __device__ __forceinline__ void stage_out(const uint32_t* sm, uint32_t* keys,
                                           uint64_t gbase, int y) {
   using TL = Tile<C>;
-  constexpr int T = TL::T, N = TL::N;
+  constexpr int T = 1 << (C - R), N = TL::N;
   __syncthreads();
   if constexpr (N / T >= 4) {
     constexpr int IT = N / 4 / T;
@@ -145,9 +145,15 @@ __device__ __forceinline__ void stage_out(const uint32_t* sm, uint32_t* keys,
   }
 }
 
-template <int C>
+template <int C, int R>
+constexpr int threads_for() {
+  return 1 << (C - R);
+}
+template <int C, int R>
 constexpr int min_blocks_for() {
-  return Tile<C>::T >= 1024 ? 1 : (1024 / Tile<C>::T > 32 ? 32 : 1024 / Tile<C>::T);
+  // a 64-register budget per thread (1024 threads per SM at full use)
+  return threads_for<C, R>() >= 1024 ? 1
+         : (1024 / threads_for<C, R>() > 32 ? 32 : 1024 / threads_for<C, R>());
 }
 
 // ---- the pass body -------------------------------------------------------------
@@ -158,10 +164,10 @@ constexpr int min_blocks_for() {
 //   tile sort, phase C     : CTA-uniform          (DL = -1, value u[C])
 //   merge, phase A         : local bit C-1 when segment B follows, else uniform
 //   merge, phase B         : uniform
-template <int C, int KIND, int SA, int SB>
+template <int C, int KIND, int SA, int SB, int RR = reg_bits(C)>
 struct PassBody {
   using S = Seq<C, KIND, SA, SB>;
-  static constexpr int R = reg_bits(C);
+  static constexpr int R = RR;
   static constexpr int NR = 1 << R;
   static constexpr int A = KIND == 0 ? C : (SB >= 0 ? SB : C);
   using RD = Rounds<S, C, R, A>;
@@ -386,7 +392,7 @@ struct PassBody {
     } else {
       constexpr int db = natural(PH) ? -1 : dloc(PH);
       const uint32_t u = (natural(PH) || db >= 0) ? 0u : uni(c, PH);
-      stage_in<C, A, db>(sm, c.keys, c.gbase, c.y, c.gin ^ u);
+      stage_in<C, A, db, R>(sm, c.keys, c.gbase, c.y, c.gin ^ u);
       L0::lds(sm, v);
     }
   }
@@ -401,7 +407,7 @@ struct PassBody {
       gstore<LL>(c, tj, v);
     } else {
       LL::sts(sm, v);
-      stage_out<C, A>(sm, c.keys, c.gbase, c.y);
+      stage_out<C, A, R>(sm, c.keys, c.gbase, c.y);
     }
   }
 
@@ -428,11 +434,11 @@ struct PassBody {
   }
 };
 
-template <int C>
-__global__ void __launch_bounds__(Tile<C>::T, min_blocks_for<C>())
+template <int C, int R = reg_bits(C)>
+__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
 tile_sort_kernel(PassParams P) {
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 0, -1, -1>;
+  using B = PassBody<C, 0, -1, -1, R>;
   typename B::Ctx c;
   c.keys = P.keys;
   c.gbase = (uint64_t)blockIdx.x << C;
@@ -444,12 +450,12 @@ tile_sort_kernel(PassParams P) {
   B::run(c, smem);
 }
 
-template <int C, int SA, int SB>
-__global__ void __launch_bounds__(Tile<C>::T, min_blocks_for<C>())
+template <int C, int SA, int SB, int R = reg_bits(C)>
+__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
 merge_kernel(PassParams P) {
   static_assert(SA >= 0 || SB >= 0, "empty pass");
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 1, SA, SB>;
+  using B = PassBody<C, 1, SA, SB, R>;
   constexpr int A = B::A;
   typename B::Ctx c;
   c.keys = P.keys;

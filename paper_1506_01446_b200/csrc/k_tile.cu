@@ -4,7 +4,18 @@
 
 namespace b200 {
 
-PassFn find_tile_kernel(int C) {
+PassFn find_tile_kernel(int C, int R) {
+  if (R == 4) {
+    switch (C) {
+      case 10: return &tile_sort_kernel<10, 4>;
+      case 11: return &tile_sort_kernel<11, 4>;
+      case 12: return &tile_sort_kernel<12, 4>;
+      case 13: return &tile_sort_kernel<13, 4>;
+      case 14: return &tile_sort_kernel<14, 4>;
+      default: return nullptr;
+    }
+  }
+  if (R != 5 && C >= 5) return nullptr;
   switch (C) {
     case 1: return &tile_sort_kernel<1>;
     case 2: return &tile_sort_kernel<2>;
@@ -28,8 +39,12 @@ PassFn find_tile_kernel(int C) {
 namespace {
 struct Tables {
   MergeTable t[kMergeCMax + 1];
+  MergeTable t4[kMergeCMax + 1];
   Tables() {
     for (auto& x : t) x = MergeTable{};
+    for (auto& x : t4) x = MergeTable{};
+    fill_merge_table_12_r4(t4[12]);
+    fill_merge_table_13_r4(t4[13]);
     fill_merge_table_11(t[11]);
     fill_merge_table_12(t[12]);
     fill_merge_table_13(t[13]);
@@ -43,9 +58,10 @@ const Tables& tables() {
 }
 }  // namespace
 
-PassFn find_merge_kernel(int C, int SA, int SB) {
+PassFn find_merge_kernel(int C, int SA, int SB, int R) {
   if (C < kMergeCMin || C > kMergeCMax) return nullptr;
-  const MergeTable& t = tables().t[C];
+  if (R != 5 && R != 4) return nullptr;
+  const MergeTable& t = R == 5 ? tables().t[C] : tables().t4[C];
   if (SB >= 0 && SA == SB - 1 && SB < 16) return t.th[SB];
   if (SA < 0 && SB >= 0 && SB < 16) return t.ho[SB];
   if (SB < 0 && SA >= 0 && SA < 16) return t.to[SA];

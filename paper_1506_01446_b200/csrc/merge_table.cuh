@@ -8,26 +8,26 @@
 
 namespace b200 {
 
-template <int C, int A>
+template <int C, int A, int R>
 PassFn th_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A, R>;
   else return nullptr;
 }
-template <int C, int A>
+template <int C, int A, int R>
 PassFn ho_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A, R>;
   else return nullptr;
 }
-template <int C, int SA>
+template <int C, int SA, int R>
 PassFn to_entry() {
-  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1>;
+  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1, R>;
   else return nullptr;
 }
-template <int C, int... I>
+template <int C, int R, int... I>
 void fill_merge_table(MergeTable& t, std::integer_sequence<int, I...>) {
-  ((t.th[I] = th_entry<C, I>()), ...);
-  ((t.ho[I] = ho_entry<C, I>()), ...);
-  ((t.to[I] = to_entry<C, I>()), ...);
+  ((t.th[I] = th_entry<C, I, R>()), ...);
+  ((t.ho[I] = ho_entry<C, I, R>()), ...);
+  ((t.to[I] = to_entry<C, I, R>()), ...);
 }
 
 }  // namespace b200
@@ -35,6 +35,13 @@ void fill_merge_table(MergeTable& t, std::integer_sequence<int, I...>) {
 #define B200_DEFINE_MERGE_TABLE(CC)                                      \
   namespace b200 {                                                       \
   void fill_merge_table_##CC(MergeTable& t) {                            \
-    fill_merge_table<CC>(t, std::make_integer_sequence<int, 16>{});      \
+    fill_merge_table<CC, 5>(t, std::make_integer_sequence<int, 16>{});   \
+  }                                                                      \
+  }
+
+#define B200_DEFINE_MERGE_TABLE_R4(CC)                                   \
+  namespace b200 {                                                       \
+  void fill_merge_table_##CC##_r4(MergeTable& t) {                       \
+    fill_merge_table<CC, 4>(t, std::make_integer_sequence<int, 16>{});   \
   }                                                                      \
   }

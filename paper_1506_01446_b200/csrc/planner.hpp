@@ -34,6 +34,7 @@ struct PlanPass {
   int segB_lo = -1, pB = 0;
   uint64_t ctas = 0;
   uint64_t ces = 0;
+  int R = 5;          // log2 keys per thread (5 = 32; 4 = 16 for latency-bound sizes)
 };
 
 struct PlanOptions {
@@ -41,6 +42,7 @@ struct PlanOptions {
   int lrun = 5;    // min contiguous run per merge pass (2^lrun keys)
   int min_ctas = 128;  // shrink the tile until the grid has this many CTAs
   int cmin = 6;    // ... but not below this tile size
+  int regbits = 0; // keys per thread = 2^regbits (0 = automatic)
 };
 
 inline int ctz64(uint64_t x) {
@@ -65,17 +67,18 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // Tile size.  With an explicit tuning (cmin == cmax) use it; otherwise the
   // per-size choice measured best on B200 (PDL between passes):
   //   k <= 12  one CTA sorts the whole array (single launch)
-  //   13..18   2^12-key tiles (latency-bound: spread over more SMs)
-  //   >= 19    2^13-key tiles: 128+ CTAs at 2^20, and at 2^24..2^28 four
-  //            CTAs per SM keep the merge passes HBM-bound (2^14-key tiles
-  //            need fewer passes but only fit two CTAs per SM and measured
-  //            slower: 12.3 vs 12.1 ms at 2^28)
+  //   13..22   2^12-key tiles: the passes are latency-bound (L2-resident
+  //            data), so more, smaller CTAs per SM win over fewer passes
+  //   >= 23    2^13-key tiles: four CTAs per SM keep the HBM-bound merge
+  //            passes streaming (2^14-key tiles need fewer passes but fit
+  //            only two CTAs per SM and measured slower: 12.3 vs 12.0 ms at
+  //            2^28)
   int C;
   if (opt.cmin == opt.cmax) {
     C = opt.cmax;
   } else if (k <= 12) {
     C = k;
-  } else if (k <= 18) {
+  } else if (k <= 22) {
     C = 12;
   } else {
     C = 13;
@@ -104,6 +107,10 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   t.ctas = total >> C;
   t.ces = (total / 2) * (uint64_t)(t.p_end * (t.p_end + 1) / 2);
   plan.push_back(t);
+  // 16 keys per thread (twice the warps per SM) up to 2^19 keys, where the
+  // passes are latency-bound; 32 keys per thread elsewhere (measured).
+  int R = opt.regbits > 0 ? opt.regbits : (k <= 19 && batch == 1 ? 4 : 5);
+  for (auto& q : plan) q.R = R;
   if (k <= C) return plan;
 
   const int lrun = opt.lrun;
@@ -112,6 +119,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   while (p <= k) {
     PlanPass m;
     m.C = C;
+    m.R = R;
     m.ctas = total >> C;
     if (b < C) {
       // Tail of phase p fits in the low bits: fuse the head of phase p+1.
