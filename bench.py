@@ -361,9 +361,17 @@ def main():
         avg_ms = fam_t[dom] / fam_n[dom]
         alg_bytes = 8 * n  # one read + one write of every key per launch
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        try:  # measured DRAM bytes per launch from the committed ncu capture
+            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+                tr = json.load(f)
+            if not batched:
+                traffic = tr.get(str(args.log2n), {}).get(dom)
+        except Exception:
+            pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": None,
+                    "traffic": traffic,
                     "algorithmic_bytes_per_launch": alg_bytes,
                     "avg_launch_ms": avg_ms,
                     "share_of_step": {f: fam_t[f] / sum(fam_t.values()) for f in fam_t}}

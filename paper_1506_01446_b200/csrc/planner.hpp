@@ -108,8 +108,11 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   t.ces = (total / 2) * (uint64_t)(t.p_end * (t.p_end + 1) / 2);
   plan.push_back(t);
   // 16 keys per thread (twice the warps per SM) up to 2^19 keys, where the
-  // passes are latency-bound; 32 keys per thread elsewhere (measured).
-  int R = opt.regbits > 0 ? opt.regbits : (k <= 19 && batch == 1 ? 4 : 5);
+  // passes are latency-bound, and for batched tiles (ALU-bound: more warps
+  // overlap the shared-memory rounds); 32 keys per thread elsewhere
+  // (measured on B200).
+  int R = opt.regbits > 0 ? opt.regbits
+                          : ((k <= 19 && batch == 1) || (batch > 1 && C >= 10 && C <= 14) ? 4 : 5);
   for (auto& q : plan) q.R = R;
   if (k <= C) return plan;
 
