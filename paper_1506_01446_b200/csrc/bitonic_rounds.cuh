@@ -91,7 +91,11 @@ constexpr bool lanes_feasible(uint32_t m) {
 // ends early when its register set would make a conflict-free lane choice
 // impossible (only enforced for C >= 10, where every residue has two
 // positions).
-template <class S, int C, int R, int A = C>
+// DF ("direct first"): round 0 stops before the first step on a bit < 5, so
+// its lanes can sit on bits 0..4 and the pass loads straight from HBM
+// instead of staging through shared memory (PassBody picks whichever cut
+// needs fewer shared-memory round trips).
+template <class S, int C, int R, int A = C, bool DF = false>
 struct Rounds {
   static constexpr bool enforce = C >= 10 && C - R >= 5;
   static constexpr int next_begin(int b) {
@@ -101,6 +105,7 @@ struct Rounds {
       const uint32_t nm = m | (1u << S::bit(i));
       if (popc(nm) > R) break;
       if (enforce && !lanes_feasible<C>(nm)) break;
+      if (DF && b == 0 && i > 0 && S::bit(i) < 5) break;
       m = nm;
       ++i;
     }

@@ -13,6 +13,8 @@
 //                              A = SB (or C when SB < 0) keys long.
 #pragma once
 
+#include <type_traits>
+
 #include "bitonic_engine.cuh"
 #include "bitonic_rounds.cuh"
 
@@ -170,7 +172,21 @@ struct PassBody {
   static constexpr int R = RR;
   static constexpr int NR = 1 << R;
   static constexpr int A = KIND == 0 ? C : (SB >= 0 ? SB : C);
-  using RD = Rounds<S, C, R, A>;
+  // Shared-memory round trips of a round cut: one per layout change, plus
+  // one for a staged load / store when the first / last layout cannot talk
+  // to HBM directly.
+  template <class RX>
+  static constexpr int smem_trips() {
+    using F = Layout<C, RX::mask(0)>;
+    using La = Layout<C, RX::mask(RX::count() - 1)>;
+    const bool dl = KIND == 1 && F::lanes_low() && A >= F::vec_bits() + 5;
+    const bool ds = KIND == 1 && La::lanes_low() && A >= La::vec_bits() + 5;
+    return (RX::count() - 1) + (dl ? 0 : 1) + (ds ? 0 : 1);
+  }
+  using RD_GREEDY = Rounds<S, C, R, A, false>;
+  using RD_DF = Rounds<S, C, R, A, true>;
+  using RD = typename std::conditional<(KIND == 1 && smem_trips<RD_DF>() < smem_trips<RD_GREEDY>()),
+                                       RD_DF, RD_GREEDY>::type;
   static constexpr int NRND = RD::count();
   template <int r>
   using L = Layout<C, RD::mask(r)>;
