@@ -112,6 +112,14 @@ int b200_bitonic_merge_split_u32(const uint32_t* local, const uint32_t* partner,
                                  uint64_t m, int keep_high, uint32_t key_xor,
                                  uint32_t* out, b200_stream_t stream);
 
+/* General two-way merge of sorted a[0..la) and b[0..lb) (same order
+ * convention as merge_split) into out[0..la+lb).  Used by the half-shard
+ * exchange of the NCCL partitioned sort: each rank merges the part of its
+ * own shard it keeps with the part of the partner shard it received. */
+int b200_bitonic_merge_u32(const uint32_t* a, uint64_t la, const uint32_t* b,
+                           uint64_t lb, uint32_t key_xor, uint32_t* out,
+                           b200_stream_t stream);
+
 /* ---- plan introspection (host only, no GPU needed) ----------------------
  * One entry per kernel launch of the sort of `batch` arrays of n keys. */
 typedef struct {

@@ -35,7 +35,7 @@ from . import _native
 __all__ = [
     "InvalidSizeError", "ConfigError", "CudaError",
     "sort_", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
-    "merge_split_", "sort_multi", "plan", "counters", "set_tuning",
+    "merge_split_", "merge_", "sort_multi", "plan", "counters", "set_tuning",
     "PassPlan", "version", "library_path",
 ]
 
@@ -181,6 +181,20 @@ def merge_split_(local, partner, out, keep_high: bool, key_xor: int = 0,
         ctypes.c_void_p(local.data_ptr()), ctypes.c_void_p(partner.data_ptr()), m,
         int(bool(keep_high)), ctypes.c_uint32(key_xor & 0xFFFFFFFF),
         ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))))
+    return out
+
+
+def merge_(a, b, out, key_xor: int = 0, stream=None):
+    """out <- merge of the sorted tensors a and b (lengths may differ; order
+    given by ``key_xor`` as in merge_split_)."""
+    for x in (a, b, out):
+        _check_tensor(x)
+    if out.numel() != a.numel() + b.numel():
+        raise ConfigError("out must hold a.numel() + b.numel() keys")
+    _check(_native.lib().b200_bitonic_merge_u32(
+        ctypes.c_void_p(a.data_ptr()), a.numel(), ctypes.c_void_p(b.data_ptr()), b.numel(),
+        ctypes.c_uint32(key_xor & 0xFFFFFFFF), ctypes.c_void_p(out.data_ptr()),
+        ctypes.c_void_p(_stream_ptr(stream))))
     return out
 
 

@@ -25,6 +25,7 @@ EXPORTED = (
     "b200_bitonic_sort_host_u32",
     "b200_bitonic_sort_u32_multi",
     "b200_bitonic_merge_split_u32",
+    "b200_bitonic_merge_u32",
     "b200_bitonic_plan",
     "b200_bitonic_run_pass_u32",
     "b200_bitonic_counters",
@@ -74,6 +75,7 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_sort_u32_multi.argtypes = [ctypes.POINTER(vp),
                                               ctypes.POINTER(ctypes.c_int), i, u64, i]
     L.b200_bitonic_merge_split_u32.argtypes = [vp, vp, u64, i, ctypes.c_uint32, vp, vp]
+    L.b200_bitonic_merge_u32.argtypes = [vp, u64, vp, u64, ctypes.c_uint32, vp, vp]
     L.b200_bitonic_plan.argtypes = [u64, u64, ctypes.POINTER(PassInfo), i,
                                     ctypes.POINTER(ctypes.c_int)]
     L.b200_bitonic_run_pass_u32.argtypes = [vp, u64, u64, i, i, vp]

@@ -235,19 +235,28 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
   return B200_OK;
 }
 
-// ---- merge-split ----------------------------------------------------------
+// ---- merge path ----------------------------------------------------------------
+// Output window [o_begin, o_begin + o_len) of merge(A[0..la), B[0..lb)).
+int merge_window_impl(const uint32_t* A, uint64_t la, const uint32_t* B, uint64_t lb,
+                      uint64_t o_begin, uint64_t o_len, uint32_t key_xor, uint32_t* out,
+                      uint64_t* scratch_coranks, cudaStream_t s) {
+  if (o_len == 0) return B200_OK;
+  const uint64_t tiles = (o_len + b200::kMergeTile - 1) / b200::kMergeTile;
+  const uint64_t nb = tiles + 1;
+  b200::merge_partition_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
+      A, la, B, lb, o_begin, o_len, key_xor, scratch_coranks, nb);
+  b200::merge_tile_kernel<<<(unsigned)tiles, b200::kMergeThreads, 0, s>>>(
+      A, la, B, lb, o_begin, o_len, key_xor, scratch_coranks, out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+  return B200_OK;
+}
+
 int merge_split_impl(const uint32_t* local, const uint32_t* partner, uint64_t m,
                      int keep_high, uint32_t key_xor, uint32_t* out,
                      uint64_t* scratch_coranks, cudaStream_t s) {
-  const uint64_t tiles = (m + b200::kMergeTile - 1) / b200::kMergeTile;
-  const uint64_t nb = tiles + 1;
-  b200::merge_partition_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
-      local, partner, m, keep_high, key_xor, scratch_coranks, nb);
-  b200::merge_tile_kernel<<<(unsigned)tiles, b200::kMergeThreads, 0, s>>>(
-      local, partner, m, keep_high, key_xor, scratch_coranks, out);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "merge-split launch");
-  return B200_OK;
+  return merge_window_impl(local, m, partner, m, keep_high ? m : 0, m, key_xor, out,
+                           scratch_coranks, s);
 }
 
 __global__ void pad_fill_kernel(uint32_t* dst, const uint32_t* src, uint64_t n,
@@ -369,6 +378,23 @@ int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending) {
 
 int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending) {
   return host_sort(h_keys, n, descending, 0u);
+}
+
+int b200_bitonic_merge_u32(const uint32_t* a, uint64_t la, const uint32_t* b,
+                           uint64_t lb, uint32_t key_xor, uint32_t* out,
+                           b200_stream_t stream) {
+  if (la + lb == 0) return B200_OK;
+  if ((la && !a) || (lb && !b) || !out) return fail(B200_CONFIG, "null pointer");
+  if ((la && out == a) || (lb && out == b)) {
+    return fail(B200_CONFIG, "out must not alias the inputs");
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t tiles = (la + lb + b200::kMergeTile - 1) / b200::kMergeTile;
+  uint64_t* cor = nullptr;
+  B200_CUDA_TRY(cudaMallocAsync(&cor, (tiles + 1) * sizeof(uint64_t), s));
+  int rc = merge_window_impl(a, la, b, lb, 0, la + lb, key_xor, out, cor, s);
+  cudaFreeAsync(cor, s);
+  return rc;
 }
 
 int b200_bitonic_merge_split_u32(const uint32_t* local, const uint32_t* partner,

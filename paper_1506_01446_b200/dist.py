@@ -12,9 +12,14 @@ becomes a merge-split (block 0-1 principle):
    direction rule as the reference's network (schedule.cpp:58-67) on shard
    indices; the lower rank of an ascending pair keeps the m smallest keys of
    the 2m union, the upper rank the m largest;
-3. the exchange moves the partner's shard over NCCL (send/recv over
-   NVLink/NVSwitch) and ``merge_split_`` (a merge-path kernel) keeps the
-   required half.
+3. the exchange moves, over NCCL send/recv (NVLink/NVSwitch), only the keys
+   the partner keeps: the split point c (how many of the lower rank's keys
+   stay low) is found with two small exchanges -- key samples every s
+   positions, then one s-key window -- after which the lower rank sends its
+   top m-c keys and the upper rank its bottom m-c keys (~m/2 each way on
+   random data: the "half-shard" exchange), and each rank merges what it
+   kept with what it received (``merge_``, a merge-path kernel).  The
+   ``exchange="full"`` mode swaps whole shards instead (NCCL baseline).
 
 Afterwards rank r holds global sorted positions [r*m, (r+1)*m).
 
@@ -62,6 +67,7 @@ class Ops:
     local_sort: Callable  # (shard, descending) -> None, in place
     merge_split: Callable  # (local, partner, out, keep_high, key_xor) -> None
     exchange: Callable  # (send, recv, partner, group) -> None
+    merge: Callable = None  # (a, b, out, key_xor) -> None (half exchange)
 
 
 def _as_wire(t):
@@ -83,23 +89,94 @@ def cuda_ops() -> Ops:
     def local_sort(t, descending):
         sort_(t, descending=descending)
 
-    def merge(local, partner, out, keep_high, kx):
+    from . import merge_
+
+    def merge_split(local, partner, out, keep_high, kx):
         merge_split_(local.view(torch.uint32), partner.view(torch.uint32),
                      out.view(torch.uint32), keep_high, kx)
 
-    return Ops(local_sort=local_sort, merge_split=merge, exchange=p2p_exchange)
+    def merge(a, b, out, kx):
+        merge_(a.view(torch.uint32), b.view(torch.uint32), out.view(torch.uint32), kx)
+
+    return Ops(local_sort=local_sort, merge_split=merge_split, exchange=p2p_exchange,
+               merge=merge)
+
+
+def _keys(t, kx):
+    """Sort-order keys of 32-bit keys as int64 (for small sample/window math)."""
+    return (t.view(torch.int32).to(torch.int64) & 0xFFFFFFFF) ^ kx
+
+
+def _split_point(cur, lower, partner, kx, group, ops, s):
+    """c = number of the lower rank's keys among the m smallest of the pair
+    (merge path diagonal m, lower rank first on ties).  Identical on both
+    ranks.  P(i) = A[i] <= B[m-1-i] (A = lower's shard, B = upper's) is
+    monotone and c is its first false index: bracket c with samples A[j*s]
+    and B[m-1-j*s], then evaluate P exactly on one window of < s indices."""
+    m = cur.numel()
+    cur = cur.view(torch.int32)  # torch has few uint32 kernels: move bits as int32
+    pos = torch.arange(0, m, s, device=cur.device)
+    nj = pos.numel()
+    # my keys as seen from both roles: from the bottom (as A), from the top (as B)
+    mine = torch.cat([cur[pos], cur[m - 1 - pos]])
+    theirs = torch.empty_like(mine)
+    ops.exchange(mine, theirs, partner, group)
+    a_s = (mine if lower else theirs)[:nj]
+    b_s = (theirs if lower else mine)[nj:]
+    p = _keys(a_s, kx) <= _keys(b_s, kx)
+    jstar = int(p.logical_not().to(torch.int32).argmax()) if bool((~p).any()) else nj
+    lo = 0 if jstar == 0 else (jstar - 1) * s + 1
+    hi = m if jstar == nj else jstar * s
+    if hi <= lo:
+        return lo
+    # window: A[lo..hi) from the lower rank, B[m-hi..m-lo) from the upper rank
+    w_mine = cur[lo:hi] if lower else cur[m - hi:m - lo]
+    w_theirs = torch.empty_like(w_mine)
+    ops.exchange(w_mine, w_theirs, partner, group)
+    a_w = w_mine if lower else w_theirs
+    b_w = (w_theirs if lower else w_mine).flip(0)  # B[m-1-i] for i = lo..hi-1
+    return lo + int((_keys(a_w, kx) <= _keys(b_w, kx)).sum())
+
+
+def _half_merge_split(cur, out, partner, keep_high, kx, group, ops, s):
+    m = cur.numel()
+    lower = not keep_high
+    c = _split_point(cur, lower, partner, kx, group, ops, s)
+    t = m - c  # keys crossing in each direction
+    if lower:
+        send, keep = cur[c:], cur[:c]
+    else:
+        send, keep = cur[:t], cur[t:]
+    recv = torch.empty(t, dtype=cur.dtype, device=cur.device)
+    if t:
+        ops.exchange(send.contiguous(), recv, partner, group)
+    if lower:
+        ops.merge(keep, recv, out, kx)
+    else:
+        ops.merge(recv, keep, out, kx)
+    return t
 
 
 def partitioned_sort_(shard: torch.Tensor, descending: bool = False, group=None,
-                      ops: Ops | None = None) -> torch.Tensor:
+                      ops: Ops | None = None, exchange: str = "half",
+                      sample_stride: int = 4096, stats: dict | None = None,
+                      rank: int | None = None, world: int | None = None) -> torch.Tensor:
     """Sort the distributed array whose slice ``shard`` this rank owns.
 
     All ranks must pass equal-length shards of the same dtype (int32 or
     uint32).  In place: ``shard`` receives this rank's slice of the result.
+    ``exchange``: "half" (only the keys the partner keeps cross the link) or
+    "full" (whole shards).  ``stats`` (optional dict) receives the number of
+    keys this rank sent per step.  ``rank``/``world`` override the process
+    group's (in-process emulation of the ranks in tests).
     """
+    if exchange not in ("half", "full"):
+        raise ValueError("exchange must be 'half' or 'full'")
     ops = ops or cuda_ops()
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if rank is None:
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
     ops.local_sort(shard, descending)
     if world == 1:
         return shard
@@ -107,11 +184,19 @@ def partitioned_sort_(shard: torch.Tensor, descending: bool = False, group=None,
     recv = torch.empty_like(shard)
     out = torch.empty_like(shard)
     cur = shard
+    sent = []
     for q, s in network_steps(world):
         partner, keep_high = step_role(rank, q, s)
-        ops.exchange(cur, recv, partner, group)
-        ops.merge_split(cur, recv, out, keep_high, kx)
+        if exchange == "half" and ops.merge is not None:
+            sent.append(_half_merge_split(cur, out, partner, keep_high, kx, group, ops,
+                                          sample_stride))
+        else:
+            ops.exchange(cur, recv, partner, group)
+            ops.merge_split(cur, recv, out, keep_high, kx)
+            sent.append(cur.numel())
         cur, out = out, cur
+    if stats is not None:
+        stats["keys_sent_per_step"] = sent
     if cur is not shard:
         shard.copy_(cur)
     return shard

@@ -37,11 +37,16 @@ def numpy_ops():
         m = local.numel()
         out.numpy()[:] = u[m:] if keep_high else u[:m]
 
+    def merge(a, b, out, kx):
+        u = np.concatenate([a.numpy(), b.numpy()])
+        out.numpy()[:] = u[np.argsort(_key(u, kx), kind="stable")]
+
     return bdist.Ops(local_sort=local_sort, merge_split=merge_split,
-                     exchange=bdist.p2p_exchange)
+                     exchange=bdist.p2p_exchange, merge=merge)
 
 
-def _worker(rank, world, port, n, dtype_name, descending, q):
+def _worker(rank, world, port, n, dtype_name, descending, q, exchange="half", stride=64,
+            shape="random"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -49,11 +54,19 @@ def _worker(rank, world, port, n, dtype_name, descending, q):
         rng = np.random.default_rng(1234)
         x = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
         x[: n // 8] = x[n // 8: n // 4]  # duplicates across shards
+        if shape == "sorted":
+            x = np.sort(x)
+        elif shape == "reversed":
+            x = np.sort(x)[::-1].copy()
+        elif shape == "equal":
+            x[:] = 7
         if dtype_name == "int32":
             x = x.view(np.int32)
         m = n // world
         shard = torch.from_numpy(x[rank * m:(rank + 1) * m].copy())
-        bdist.partitioned_sort_(shard, descending=descending, ops=numpy_ops())
+        stats = {}
+        bdist.partitioned_sort_(shard, descending=descending, ops=numpy_ops(),
+                                exchange=exchange, sample_stride=stride, stats=stats)
         wire = shard.view(torch.int32)  # gloo has no uint32 collectives
         parts = [torch.empty_like(wire) for _ in range(world)]
         dist.all_gather(parts, wire)
@@ -62,27 +75,47 @@ def _worker(rank, world, port, n, dtype_name, descending, q):
             want = np.sort(x)
             if descending:
                 want = want[::-1]
-            q.put(bool((got == want).all()))
+            q.put((bool((got == want).all()), stats.get("keys_sent_per_step")))
     finally:
         dist.destroy_process_group()
+
+
+def _run(world, dtype_name, descending, exchange="half", stride=64, shape="random",
+         n=1 << 12):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, dtype_name, descending, q,
+                                               exchange, stride, shape))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    return q.get(timeout=5)
 
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("dtype_name,descending", [("uint32", False), ("int32", False),
                                                     ("uint32", True)])
 def test_partitioned_sort_gloo(world, dtype_name, descending):
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    n = 1 << 12
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, dtype_name, descending, q))
-             for r in range(world)]
-    for p in procs:
-        p.start()
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    assert q.get(timeout=5) is True
+    ok, sent = _run(world, dtype_name, descending)
+    assert ok
+    # the half exchange moves about half a shard per step on random data
+    m = (1 << 12) // world
+    assert all(0 <= t <= m for t in sent) and sum(sent) < len(sent) * m * 0.8
+
+
+@pytest.mark.parametrize("shape", ["sorted", "reversed", "equal"])
+def test_partitioned_sort_gloo_adversarial(shape):
+    ok, _ = _run(4, "uint32", False, shape=shape, stride=16)
+    assert ok
+
+
+def test_partitioned_sort_gloo_full_exchange():
+    ok, sent = _run(2, "int32", True, exchange="full")
+    assert ok and sent == [(1 << 12) // 2]
 
 
 def test_schedule_roles():
