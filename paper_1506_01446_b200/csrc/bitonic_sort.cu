@@ -56,6 +56,7 @@ b200::PlanOptions plan_options() {
   }
   o.lrun = g_min_run_bits.load();
   if (const char* e = std::getenv("B200_BITONIC_REGBITS")) o.regbits = std::atoi(e);
+  if (const char* e = std::getenv("B200_BITONIC_PLANNER")) o.dp = std::strcmp(e, "greedy") != 0;
   return o;
 }
 
@@ -166,15 +167,16 @@ struct PlanKey {
   int k;
   uint64_t batch;
   int cmax, cmin, lrun, min_ctas, regbits;
+  bool dp;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
-           lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits;
+           lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
-  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits};
+  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.dp};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;

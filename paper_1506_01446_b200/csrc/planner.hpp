@@ -19,6 +19,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -37,12 +38,98 @@ struct PlanPass {
   int R = 5;          // log2 keys per thread (5 = 32; 4 = 16 for latency-bound sizes)
 };
 
+// ---- cost model: shared-memory round trips of one merge pass ---------------
+// Mirrors the kernels' compile-time round cutting (bitonic_rounds.cuh:
+// Rounds, Layout::lanes_low; bitonic_static.cuh: PassBody::smem_trips) so
+// the planner can prefer pass shapes that load/store HBM directly.
+namespace detail {
+
+inline int popcount32(uint32_t x) {
+  int c = 0;
+  while (x) {
+    c += x & 1u;
+    x >>= 1;
+  }
+  return c;
+}
+
+inline bool lanes_feasible(int C, uint32_t m) {
+  for (int r = 0; r < 5; ++r) {
+    bool ok = false;
+    for (int p = r; p < C; p += 5)
+      if (!(m & (1u << p))) ok = true;
+    if (!ok) return false;
+  }
+  return true;
+}
+
+inline std::vector<uint32_t> cut_rounds(const std::vector<int>& bits, int C, int R, int A,
+                                        bool DF) {
+  const bool enforce = C >= 10 && C - R >= 5;
+  std::vector<uint32_t> masks;
+  size_t i = 0;
+  while (i < bits.size()) {
+    uint32_t m = 0;
+    const size_t b = i;
+    while (i < bits.size()) {
+      const uint32_t nm = m | (1u << bits[i]);
+      if (popcount32(nm) > R) break;
+      if (enforce && !lanes_feasible(C, nm)) break;
+      if (DF && b == 0 && i > 0 && bits[i] < 5) break;
+      m = nm;
+      ++i;
+    }
+    for (int x = A - 1; x >= 5 && popcount32(m) < R; --x) {
+      if (m & (1u << x)) continue;
+      if (enforce && !lanes_feasible(C, m | (1u << x))) continue;
+      m |= 1u << x;
+    }
+    for (int x = C - 1; x >= 0 && popcount32(m) < R; --x) {
+      if (m & (1u << x)) continue;
+      if (enforce && !lanes_feasible(C, m | (1u << x))) continue;
+      m |= 1u << x;
+    }
+    masks.push_back(m);
+  }
+  return masks;
+}
+
+inline bool direct(int C, int R, int A, uint32_t m) {
+  int v = 0;
+  while (v < C && (m & (1u << v))) ++v;
+  if (C - R < 5 || v > 2 || v + 5 > C) return false;
+  for (int b = v; b < v + 5; ++b)
+    if (m & (1u << b)) return false;
+  return A >= v + 5;
+}
+
+// Shared-memory round trips of merge pass (SA, SB) on a 2^C tile.
+inline int merge_trips(int C, int R, int SA, int SB) {
+  const int A = SB >= 0 ? SB : C;
+  std::vector<int> bits;
+  for (int b = SA; b >= 0; --b) bits.push_back(b);
+  if (SB >= 0)
+    for (int b = C - 1; b >= SB; --b) bits.push_back(b);
+  int best = 1 << 20;
+  for (bool df : {false, true}) {
+    const auto m = cut_rounds(bits, C, R, A, df);
+    const int t = (int)m.size() - 1 + (direct(C, R, A, m.front()) ? 0 : 1) +
+                  (direct(C, R, A, m.back()) ? 0 : 1);
+    if (t < best) best = t;
+  }
+  return best;
+}
+
+}  // namespace detail
+
 struct PlanOptions {
   int cmax = 15;   // largest tile (2^cmax keys per CTA)
   int lrun = 5;    // min contiguous run per merge pass (2^lrun keys)
   int min_ctas = 128;  // shrink the tile until the grid has this many CTAs
   int cmin = 6;    // ... but not below this tile size
   int regbits = 0; // keys per thread = 2^regbits (0 = automatic)
+  bool dp = true;  // cost-model planner (false: greedy packing)
+  double trip_cost = 0.10;  // extra cost of a shared-memory round trip, in passes
 };
 
 inline int ctz64(uint64_t x) {
@@ -117,48 +204,123 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   if (k <= C) return plan;
 
   const int lrun = opt.lrun;
-  int p = C + 1;  // current phase
-  int b = C;      // next step bit of phase p (steps run b, b-1, ..., 0)
-  while (p <= k) {
+  auto push_tail_head = [&](int p, int b, int h) {
     PlanPass m;
     m.C = C;
     m.R = R;
     m.ctas = total >> C;
+    m.segA_hi = b;
+    m.pA = p;
+    if (h > 0) {
+      m.a = C - h;
+      m.y = p - h + 1;
+      m.segB_lo = m.a;
+      m.pB = p + 1;
+      m.ces = (total / 2) * (uint64_t)((b + 1) + h);
+    } else {
+      m.a = C;
+      m.y = C;
+      m.ces = (total / 2) * (uint64_t)(b + 1);
+    }
+    plan.push_back(m);
+  };
+  auto push_middle = [&](int p, int b, int h) {
+    PlanPass m;
+    m.C = C;
+    m.R = R;
+    m.ctas = total >> C;
+    m.a = C - h;
+    m.y = b - h + 1;
+    m.segB_lo = m.a;
+    m.pB = p;
+    m.ces = (total / 2) * (uint64_t)h;
+    plan.push_back(m);
+  };
+
+  if (opt.dp) {
+    // Dynamic program over (phase p, next step bit b): each pass costs 1 plus
+    // trip_cost per extra shared-memory round trip; shapes are restricted to
+    // the instantiated kernel families (tail-only, tail+head with a = b+1,
+    // middle runs of h high bits).
+    const int K = k + 2;
+    std::vector<double> best((size_t)K * K, -1.0);
+    std::vector<int> choice((size_t)K * K, 0);  // 0 tail-only, >0 tail+head h, <0 middle -h
+    auto cost_of = [&](int SA, int SB) {
+      return 1.0 + opt.trip_cost * (detail::merge_trips(C, R, SA, SB) - 1);
+    };
+    std::function<double(int, int)> solve = [&](int p, int b) -> double {
+      if (p > k) return 0.0;
+      double& memo = best[(size_t)p * K + b];
+      if (memo >= 0) return memo;
+      double bc = 1e30;
+      int bch = 0;
+      if (b < C) {
+        const double t0 = cost_of(b, -1) + solve(p + 1, p);
+        bc = t0;
+        bch = 0;
+        const int h = C - (b + 1);
+        if (p < k && b + 1 >= lrun && h >= 1) {
+          const double t1 = cost_of(b, b + 1) + solve(p + 1, p - h);
+          if (t1 < bc) {
+            bc = t1;
+            bch = h;
+          }
+        }
+      } else {
+        for (int h = 1; h <= C - lrun && h <= b; ++h) {
+          const double t = cost_of(-1, C - h) + solve(p, b - h);
+          if (t < bc - 1e-9) {
+            bc = t;
+            bch = -h;
+          }
+        }
+      }
+      choice[(size_t)p * K + b] = bch;
+      memo = bc;
+      return bc;
+    };
+    solve(C + 1, C);
+    int p = C + 1, b = C;
+    while (p <= k) {
+      const int ch = choice[(size_t)p * K + b];
+      if (b < C) {
+        push_tail_head(p, b, ch);
+        if (ch > 0) {
+          b = p - ch;
+          p = p + 1;
+        } else {
+          p = p + 1;
+          b = p - 1;
+        }
+      } else {
+        push_middle(p, b, -ch);
+        b -= -ch;
+      }
+    }
+    return plan;
+  }
+
+  int p = C + 1;  // current phase
+  int b = C;      // next step bit of phase p (steps run b, b-1, ..., 0)
+  while (p <= k) {
     if (b < C) {
       // Tail of phase p fits in the low bits: fuse the head of phase p+1.
       const int low = (b + 1 > lrun) ? b + 1 : lrun;
       int h = C - low;
       if (p == k) h = 0;
-      m.segA_hi = b;
-      m.pA = p;
+      push_tail_head(p, b, h > 0 ? h : 0);
       if (h > 0) {
-        m.a = C - h;
-        m.y = p - h + 1;
-        m.segB_lo = m.a;
-        m.pB = p + 1;
-        m.ces = (total / 2) * (uint64_t)((b + 1) + h);
-        plan.push_back(m);
         b = p - h;  // next step bit of phase p+1
         p = p + 1;
       } else {
-        m.a = C;
-        m.y = C;
-        m.ces = (total / 2) * (uint64_t)(b + 1);
-        plan.push_back(m);
         p = p + 1;
         b = p - 1;
       }
     } else {
       // Middle of phase p: h high bits b..b-h+1 plus a coalescing run.
       int h = C - lrun;
-      // Do not take more than leaves a non-empty remainder.
       if (h > b) h = b;
-      m.a = C - h;
-      m.y = b - h + 1;
-      m.segB_lo = m.a;
-      m.pB = p;
-      m.ces = (total / 2) * (uint64_t)h;
-      plan.push_back(m);
+      push_middle(p, b, h);
       b -= h;
     }
   }
