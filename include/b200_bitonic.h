@@ -71,6 +71,15 @@ int b200_bitonic_sort_i32_batched(int32_t* d_keys, uint64_t n_per_array,
                                   uint64_t batch, int descending,
                                   b200_stream_t stream);
 
+/* float32 keys (the paper's future-work key types): sorted
+ * by IEEE-754 totalOrder -- -NaN < -inf < ... < -0.0 < +0.0 < ... < +inf <
+ * +NaN -- via the order-preserving bit map f -> f ^ (sign ? ~0 : 0x80000000)
+ * applied before and undone after the uint32 network (two elementwise
+ * passes).  n must be a power of two >= 2; use b200_bitonic_sort_padded_*
+ * semantics via the Python sort_padded_ for other lengths. */
+int b200_bitonic_sort_f32(float* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream);
+
 /* Any length n >= 1 (the reference's pad_to_pow2 + sort + truncate,
  * bench.cpp:366-377, acceptance.cpp:114-156): when n is not a power of two
  * the keys are copied into a stream-ordered scratch buffer of bit_ceil(n)

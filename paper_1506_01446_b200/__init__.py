@@ -86,7 +86,9 @@ def _key_dtype(t):
         return "i32"
     if t.dtype == torch.uint32:
         return "u32"
-    raise ConfigError(f"keys must be int32 or uint32, got {t.dtype}")
+    if t.dtype == torch.float32:
+        return "f32"
+    raise ConfigError(f"keys must be int32, uint32 or float32, got {t.dtype}")
 
 
 def _check_tensor(t) -> None:
@@ -97,11 +99,13 @@ def _check_tensor(t) -> None:
 
 
 def sort_(t, descending: bool = False, stream=None):
-    """Sort a 1-D CUDA tensor of int32 (signed order, the reference's key type)
-    or uint32 keys in place; asynchronous on ``stream`` (default: current)."""
+    """Sort a 1-D CUDA tensor of int32 (signed order, the reference's key type),
+    uint32, or float32 (IEEE totalOrder) keys in place; asynchronous on
+    ``stream`` (default: current)."""
     _check_tensor(t)
     kind = _key_dtype(t)
-    fn = _native.lib().b200_bitonic_sort_i32 if kind == "i32" else _native.lib().b200_bitonic_sort_u32
+    fn = {"i32": _native.lib().b200_bitonic_sort_i32, "u32": _native.lib().b200_bitonic_sort_u32,
+          "f32": _native.lib().b200_bitonic_sort_f32}[kind]
     _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
               ctypes.c_void_p(_stream_ptr(stream))))
     return t
@@ -113,6 +117,8 @@ def sort_padded_(t, descending: bool = False, stream=None):
     buffer (stream-ordered allocation); powers of two sort in place."""
     _check_tensor(t)
     kind = _key_dtype(t)
+    if kind == "f32":
+        raise ConfigError("float32 keys: use sort_")
     fn = (_native.lib().b200_bitonic_sort_padded_i32 if kind == "i32"
           else _native.lib().b200_bitonic_sort_padded_u32)
     _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
@@ -126,6 +132,8 @@ def sort_batched_(t, n_per_array: int, descending: bool = False, stream=None):
     if n_per_array < 1 or t.numel() % n_per_array:
         raise ConfigError("numel must be a multiple of n_per_array")
     kind = _key_dtype(t)
+    if kind == "f32":
+        raise ConfigError("float32 keys: use sort_")
     fn = (_native.lib().b200_bitonic_sort_i32_batched if kind == "i32"
           else _native.lib().b200_bitonic_sort_u32_batched)
     _check(fn(ctypes.c_void_p(t.data_ptr()), n_per_array, t.numel() // n_per_array,

@@ -261,6 +261,19 @@ int merge_split_impl(const uint32_t* local, const uint32_t* partner, uint64_t m,
                            scratch_coranks, s);
 }
 
+// float32 <-> order-preserving uint32 (IEEE totalOrder)
+__global__ void f32_to_key_kernel(uint32_t* d, uint64_t n, int inverse) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t x = d[i];
+    if (!inverse) {
+      d[i] = x ^ ((uint32_t)((int32_t)x >> 31) | 0x80000000u);
+    } else {
+      d[i] = x ^ ((uint32_t)((int32_t)~x >> 31) | 0x80000000u);
+    }
+  }
+}
+
 __global__ void pad_fill_kernel(uint32_t* dst, const uint32_t* src, uint64_t n,
                                 uint64_t m, uint32_t pad) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -305,6 +318,24 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
 }  // namespace
 
 extern "C" {
+
+int b200_bitonic_sort_f32(float* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream) {
+  if (n < 2 || !is_pow2(n)) {
+    return fail(B200_INVALID_SIZE,
+                "length must be a power of two >= 2, got " + std::to_string(n));
+  }
+  if (d_keys == nullptr) return fail(B200_CONFIG, "null key pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint32_t* d = reinterpret_cast<uint32_t*>(d_keys);
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  f32_to_key_kernel<<<grid, 256, 0, s>>>(d, n, 0);
+  int rc = sort_impl(d, n, 1, descending, 0u, s);
+  f32_to_key_kernel<<<grid, 256, 0, s>>>(d, n, 1);
+  cudaError_t e = cudaGetLastError();
+  if (rc == B200_OK && e != cudaSuccess) rc = cuda_fail(e, "f32 key transform");
+  return rc;
+}
 
 int b200_bitonic_sort_padded_u32(uint32_t* d_keys, uint64_t n, int descending,
                                  b200_stream_t stream) {
