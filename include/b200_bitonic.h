@@ -71,6 +71,20 @@ int b200_bitonic_sort_i32_batched(int32_t* d_keys, uint64_t n_per_array,
                                   uint64_t batch, int descending,
                                   b200_stream_t stream);
 
+/* Key-value sort: d_vals[i] (a 32-bit payload) moves with d_keys[i].  The
+ * network is the reference's exactly (same compare-exchange pairs and
+ * directions, swap only when strictly out of order, engine.cpp:16-22), so
+ * the payload order of equal keys is the reference network's own -- not
+ * stable, but bit-identical to sequential_bitonic_sort carrying a payload.
+ * n must be a power of two >= 2; both pointers 16-byte aligned. */
+int b200_bitonic_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, uint64_t n,
+                                int descending, b200_stream_t stream);
+int b200_bitonic_sort_pairs_i32(int32_t* d_keys, uint32_t* d_vals, uint64_t n,
+                                int descending, b200_stream_t stream);
+int b200_bitonic_sort_pairs_u32_batched(uint32_t* d_keys, uint32_t* d_vals,
+                                        uint64_t n_per_array, uint64_t batch,
+                                        int descending, b200_stream_t stream);
+
 /* float32 keys (the paper's future-work key types): sorted
  * by IEEE-754 totalOrder -- -NaN < -inf < ... < -0.0 < +0.0 < ... < +inf <
  * +NaN -- via the order-preserving bit map f -> f ^ (sign ? ~0 : 0x80000000)

@@ -55,6 +55,8 @@ class Oracle:
         lib.oracle_bitonic_u32.argtypes = [_u32p, ctypes.c_uint64, ctypes.c_int]
         lib.oracle_bitonic_batched_u32.argtypes = [_u32p, ctypes.c_uint64,
                                                    ctypes.c_uint64, ctypes.c_int]
+        lib.oracle_bitonic_pairs.argtypes = [_u32p, _u32p, ctypes.c_uint64, ctypes.c_int,
+                                             ctypes.c_uint32]
         lib.oracle_quicksort_i32.argtypes = [_i32p, ctypes.c_uint64]
         lib.oracle_quicksort_i32.restype = None
         lib.oracle_quicksort_u32.argtypes = [_u32p, ctypes.c_uint64, ctypes.c_int]
@@ -95,6 +97,17 @@ class Oracle:
                                                a.size // n_per, int(descending)):
             raise ValueError("length must be a power of two >= 2")
         return a
+
+    def bitonic_pairs(self, keys: np.ndarray, values: np.ndarray, descending: bool = False):
+        """The reference network with a payload moved on every swap.  keys may
+        be int32 (signed order) or uint32."""
+        kx = 0x80000000 if keys.dtype == np.int32 else 0
+        k = np.ascontiguousarray(keys).view(np.uint32).copy()
+        v = np.ascontiguousarray(values, dtype=np.uint32).copy()
+        if self.lib.oracle_bitonic_pairs(_ptr(k, _u32p), _ptr(v, _u32p), k.size,
+                                         int(descending), kx):
+            raise ValueError("length must be a power of two >= 2")
+        return k.view(keys.dtype), v
 
     def quicksort_i32(self, keys: np.ndarray) -> np.ndarray:
         a = np.ascontiguousarray(keys, dtype=np.int32).copy()

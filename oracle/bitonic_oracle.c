@@ -154,6 +154,39 @@ int oracle_bitonic_u32(uint32_t* a, uint64_t n, int descending) {
   return ORACLE_OK;
 }
 
+/* Key-value: the same network (engine.cpp:248-266) with a 32-bit payload
+ * moved alongside every key swap.  compare_exchange swaps only when strictly
+ * out of order (engine.cpp:16-22), so the payload order of equal keys is the
+ * network's own (not stable) -- the GPU kernels must reproduce it exactly.
+ * key_xor: 0 = uint32 order, 0x80000000 = int32 order. */
+int oracle_bitonic_pairs(uint32_t* k, uint32_t* v, uint64_t n, int descending,
+                         uint32_t key_xor) {
+  if (!is_pow2_ge2(n)) return ORACLE_INVALID_SIZE;
+  unsigned lg = 0;
+  while ((1ULL << lg) < n) ++lg;
+  for (unsigned phase = 1; phase <= lg; ++phase) {
+    const uint64_t span = 1ULL << phase;
+    for (unsigned step = phase; step >= 1; --step) {
+      const uint64_t stride = 1ULL << (step - 1);
+      for (uint64_t t = 0; t < n / 2; ++t) {
+        const uint64_t i = pair_base(t, stride);
+        int asc = (i & span) == 0;
+        if (descending) asc = !asc;
+        const uint32_t x = k[i] ^ key_xor, y = k[i + stride] ^ key_xor;
+        if (asc ? (x > y) : (x < y)) {
+          uint32_t tk = k[i];
+          k[i] = k[i + stride];
+          k[i + stride] = tk;
+          uint32_t tv = v[i];
+          v[i] = v[i + stride];
+          v[i + stride] = tv;
+        }
+      }
+    }
+  }
+  return ORACLE_OK;
+}
+
 /* Batched: `batch` contiguous arrays of n_per keys, each sorted on its own. */
 int oracle_bitonic_batched_u32(uint32_t* a, uint64_t n_per, uint64_t batch,
                                int descending) {

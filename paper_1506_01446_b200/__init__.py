@@ -34,7 +34,7 @@ from . import _native
 
 __all__ = [
     "InvalidSizeError", "ConfigError", "CudaError",
-    "sort_", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
+    "sort_", "sort_pairs_", "argsort", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
     "merge_split_", "merge_", "sort_multi", "plan", "counters", "set_tuning",
     "PassPlan", "version", "library_path",
 ]
@@ -109,6 +109,35 @@ def sort_(t, descending: bool = False, stream=None):
     _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
               ctypes.c_void_p(_stream_ptr(stream))))
     return t
+
+
+def sort_pairs_(keys, values, descending: bool = False, stream=None):
+    """Key-value sort in place: ``values`` (a 32-bit payload tensor of the same
+    length) moves with ``keys`` (int32 or uint32).  Same network and tie rule
+    as the reference (swap only when strictly out of order): equal keys keep
+    the reference network's payload order (not stable)."""
+    import torch
+    _check_tensor(keys)
+    _check_tensor(values)
+    if values.numel() != keys.numel() or values.element_size() != 4:
+        raise ConfigError("values must be a 32-bit tensor with one entry per key")
+    kind = _key_dtype(keys)
+    if kind == "f32":
+        raise ConfigError("key-value sort takes int32 or uint32 keys")
+    fn = (_native.lib().b200_bitonic_sort_pairs_i32 if kind == "i32"
+          else _native.lib().b200_bitonic_sort_pairs_u32)
+    _check(fn(ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
+              keys.numel(), int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
+    return keys, values
+
+
+def argsort(keys, descending: bool = False, stream=None):
+    """Indices that sort ``keys`` (not modified), via the key-value network."""
+    import torch
+    k = keys.clone()
+    idx = torch.arange(keys.numel(), dtype=torch.int32, device=keys.device)
+    sort_pairs_(k, idx, descending=descending, stream=stream)
+    return idx
 
 
 def sort_padded_(t, descending: bool = False, stream=None):

@@ -19,6 +19,9 @@ EXPORTED = (
     "b200_bitonic_sort_i32",
     "b200_bitonic_sort_u32_batched",
     "b200_bitonic_sort_i32_batched",
+    "b200_bitonic_sort_pairs_u32",
+    "b200_bitonic_sort_pairs_i32",
+    "b200_bitonic_sort_pairs_u32_batched",
     "b200_bitonic_sort_f32",
     "b200_bitonic_sort_padded_u32",
     "b200_bitonic_sort_padded_i32",
@@ -70,6 +73,9 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_sort_u32_batched.argtypes = [vp, u64, u64, i, vp]
     L.b200_bitonic_sort_i32_batched.argtypes = [vp, u64, u64, i, vp]
     L.b200_bitonic_sort_f32.argtypes = [vp, u64, i, vp]
+    L.b200_bitonic_sort_pairs_u32.argtypes = [vp, vp, u64, i, vp]
+    L.b200_bitonic_sort_pairs_i32.argtypes = [vp, vp, u64, i, vp]
+    L.b200_bitonic_sort_pairs_u32_batched.argtypes = [vp, vp, u64, u64, i, vp]
     L.b200_bitonic_sort_padded_u32.argtypes = [vp, u64, i, vp]
     L.b200_bitonic_sort_padded_i32.argtypes = [vp, u64, i, vp]
     L.b200_bitonic_sort_host_i32.argtypes = [vp, u64, i]

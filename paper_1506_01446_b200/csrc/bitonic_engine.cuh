@@ -66,6 +66,7 @@ __host__ __device__ constexpr int tile_threads(int C) {
 // the planner (planner.cpp) and passed by value.
 struct PassParams {
   uint32_t* keys;     // whole array (all batches), in place
+  uint32_t* vals;     // payloads moved with the keys (key-value kernels only)
   uint32_t gmask_in;  // XOR applied at load  (key order transform, first pass)
   uint32_t gmask_out; // XOR applied at store (inverse transform, last pass)
   int a;              // local bits [0,a) -> global bits [0,a)

@@ -323,6 +323,48 @@ struct Layout {
       }
     }
   }
+  // Key-value CE: keys as ce<B>; the payload follows its key.  The swap
+  // happens only when strictly out of order (compare_exchange,
+  // engine.cpp:16-22), so equal keys keep their payloads in place -- the
+  // reference network's own payload order.
+  template <int B>
+  __device__ __forceinline__ static void ce_kv(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+    constexpr int q = qof(B);
+    static_assert(q >= 0, "CE bit must be a register bit");
+#pragma unroll
+    for (int e = 0; e < NR; ++e) {
+      if (!(e & (1 << q))) {
+        const int f = e | (1 << q);
+        const uint32_t x = v[e], y = v[f];
+        const bool sw = x > y;
+        v[e] = min(x, y);
+        v[f] = max(x, y);
+        const uint32_t a = w[e], b = w[f];
+        w[e] = sw ? b : a;
+        w[f] = sw ? a : b;
+      }
+    }
+  }
+  template <int B, int D>
+  __device__ __forceinline__ static void ce_dir_kv(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+    constexpr int q = qof(B);
+    constexpr int qd = qof(D);
+    static_assert(q >= 0 && qd >= 0, "CE and direction bits must be register bits");
+#pragma unroll
+    for (int e = 0; e < NR; ++e) {
+      if (!(e & (1 << q))) {
+        const int f = e | (1 << q);
+        const uint32_t x = v[e], y = v[f];
+        const bool desc = (e >> qd) & 1;
+        const bool sw = desc ? (x < y) : (x > y);
+        v[e] = desc ? max(x, y) : min(x, y);
+        v[f] = desc ? min(x, y) : max(x, y);
+        const uint32_t a = w[e], b = w[f];
+        w[e] = sw ? b : a;
+        w[f] = sw ? a : b;
+      }
+    }
+  }
   // XOR register e with all-ones when bit LB of its local index is set
   // (LB a register bit) -- or with the per-thread uniform u when LB is a
   // thread bit -- or with u when LB < 0 (uniform source).

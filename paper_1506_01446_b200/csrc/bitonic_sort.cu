@@ -103,7 +103,12 @@ std::atomic<int> g_pdl{1};  // programmatic dependent launch between passes
 // Returns the kernel and its keys-per-thread exponent (the block size is
 // 2^(C - R)).  Shapes without a 16-keys-per-thread instantiation fall back to
 // 32 keys per thread.
-b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out) {
+b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out, bool kv) {
+  if (kv) {
+    *R_out = q.R;
+    return q.tile_sort ? (q.p_end == q.C ? b200::find_tile_kernel(q.C, q.R, true) : nullptr)
+                       : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo, q.R, true);
+  }
   if (!g_force_generic.load()) {
     for (int R : {q.R, 5}) {
       b200::PassFn f = q.tile_sort
@@ -123,8 +128,8 @@ b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out) {
 std::mutex g_attr_mu;
 std::vector<std::vector<const void*>> g_attr_done;
 
-cudaError_t ensure_attr(const void* fn, int C) {
-  const int bytes = b200::tile_smem_words(C) * 4;
+cudaError_t ensure_attr(const void* fn, int C, int arrays) {
+  const int bytes = b200::tile_smem_words(C) * 4 * arrays;
   if (bytes <= 48 * 1024) return cudaSuccess;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -141,11 +146,13 @@ cudaError_t ensure_attr(const void* fn, int C) {
 cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
                         cudaStream_t s) {
   int R = 5;
-  b200::PassFn f = select_kernel(q, &R);
+  const bool kv = p.vals != nullptr;
+  b200::PassFn f = select_kernel(q, &R, kv);
+  if (f == nullptr) return cudaErrorNotSupported;  // no such key-value shape
   const void* fn = reinterpret_cast<const void*>(f);
-  cudaError_t e = ensure_attr(fn, q.C);
+  cudaError_t e = ensure_attr(fn, q.C, kv ? 2 : 1);
   if (e != cudaSuccess) return e;
-  const size_t smem = (size_t)b200::tile_smem_words(q.C) * 4;
+  const size_t smem = (size_t)b200::tile_smem_words(q.C) * 4 * (kv ? 2 : 1);
   void* args[] = {&p};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)q.ctas);
@@ -167,16 +174,17 @@ struct PlanKey {
   int k;
   uint64_t batch;
   int cmax, cmin, lrun, min_ctas, regbits;
-  bool dp;
+  bool dp, kv;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
-           lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp;
+           lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp &&
+           kv == o.kv;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
-  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.dp};
+  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.dp, o.kv};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;
@@ -189,7 +197,8 @@ std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanO
 // Validates and runs the whole plan (or only pass `only`, when >= 0).
 // key_xor: 0x80000000 for int32 keys.
 int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
-              uint32_t key_xor, cudaStream_t stream, int only = -1) {
+              uint32_t key_xor, cudaStream_t stream, int only = -1,
+              uint32_t* d_vals = nullptr) {
   if (n_per < 2 || !is_pow2(n_per)) {
     return fail(B200_INVALID_SIZE,
                 "length must be a power of two >= 2, got " +
@@ -205,13 +214,16 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
   }
   if (d_keys == nullptr) return fail(B200_CONFIG, "null key pointer");
   std::vector<b200::PlanPass> plan;
+  b200::PlanOptions popt = plan_options();
+  popt.kv = d_vals != nullptr;
   try {
-    plan = cached_plan(k, batch, plan_options());
+    plan = cached_plan(k, batch, popt);
   } catch (const std::exception& e) {
     return fail(B200_CONFIG, e.what());
   }
-  if (plan.front().C >= 2 && (reinterpret_cast<uintptr_t>(d_keys) & 15u) != 0) {
-    return fail(B200_CONFIG, "device pointer must be 16-byte aligned");
+  if (plan.front().C >= 2 && ((reinterpret_cast<uintptr_t>(d_keys) & 15u) != 0 ||
+                                (reinterpret_cast<uintptr_t>(d_vals) & 15u) != 0)) {
+    return fail(B200_CONFIG, "device pointers must be 16-byte aligned");
   }
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
   if (only >= (int)plan.size()) return fail(B200_CONFIG, "pass index outside the plan");
@@ -220,6 +232,7 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     const b200::PlanPass& q = plan[i];
     b200::PassParams p{};
     p.keys = d_keys;
+    p.vals = d_vals;
     p.gmask_in = (i == 0) ? gmask : 0u;
     p.gmask_out = (i + 1 == plan.size()) ? gmask : 0u;
     p.a = q.a;
@@ -232,6 +245,9 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     p.segB_lo = q.segB_lo;
     p.pB = q.pB;
     cudaError_t e = launch_pass(q, p, stream);
+    if (e == cudaErrorNotSupported) {
+      return fail(B200_CONFIG, "no key-value kernel for this tile size (use tile_bits 0, 12 or 13)");
+    }
     if (e != cudaSuccess) return cuda_fail(e, "bitonic pass launch");
   }
   return B200_OK;
@@ -318,6 +334,28 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
 }  // namespace
 
 extern "C" {
+
+int b200_bitonic_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, uint64_t n,
+                                int descending, b200_stream_t stream) {
+  if (d_vals == nullptr) return fail(B200_CONFIG, "null value pointer");
+  return sort_impl(d_keys, n, 1, descending, 0u, reinterpret_cast<cudaStream_t>(stream), -1,
+                   d_vals);
+}
+
+int b200_bitonic_sort_pairs_i32(int32_t* d_keys, uint32_t* d_vals, uint64_t n,
+                                int descending, b200_stream_t stream) {
+  if (d_vals == nullptr) return fail(B200_CONFIG, "null value pointer");
+  return sort_impl(reinterpret_cast<uint32_t*>(d_keys), n, 1, descending, 0x80000000u,
+                   reinterpret_cast<cudaStream_t>(stream), -1, d_vals);
+}
+
+int b200_bitonic_sort_pairs_u32_batched(uint32_t* d_keys, uint32_t* d_vals,
+                                        uint64_t n_per_array, uint64_t batch,
+                                        int descending, b200_stream_t stream) {
+  if (d_vals == nullptr) return fail(B200_CONFIG, "null value pointer");
+  return sort_impl(d_keys, n_per_array, batch, descending, 0u,
+                   reinterpret_cast<cudaStream_t>(stream), -1, d_vals);
+}
 
 int b200_bitonic_sort_f32(float* d_keys, uint64_t n, int descending,
                           b200_stream_t stream) {

@@ -166,7 +166,7 @@ constexpr int min_blocks_for() {
 //   tile sort, phase C     : CTA-uniform          (DL = -1, value u[C])
 //   merge, phase A         : local bit C-1 when segment B follows, else uniform
 //   merge, phase B         : uniform
-template <int C, int KIND, int SA, int SB, int RR = reg_bits(C)>
+template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), bool KV = false>
 struct PassBody {
   using S = Seq<C, KIND, SA, SB>;
   static constexpr int R = RR;
@@ -202,6 +202,7 @@ struct PassBody {
 
   struct Ctx {
     uint32_t* keys;
+    uint32_t* vals;       // payloads (KV)
     uint64_t gbase;
     int y;
     uint32_t uA, uB;      // uniform direction masks (merge)
@@ -319,28 +320,27 @@ struct PassBody {
   }
 
   template <class LR, int I>
-  __device__ __forceinline__ static void one_step(uint32_t (&v)[NR]) {
+  __device__ __forceinline__ static void one_step(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
     constexpr int ph = S::phase(I);
     constexpr int b = S::bit(I);
-    if constexpr (natural(ph)) {
-      if constexpr (ph == 0) {
-        LR::template ce<b>(v);
-      } else {
-        LR::template ce_dir<b, ph>(v);
-      }
+    if constexpr (natural(ph) && ph != 0) {
+      if constexpr (KV) LR::template ce_dir_kv<b, ph>(v, w);
+      else LR::template ce_dir<b, ph>(v);
     } else {
-      LR::template ce<b>(v);
+      if constexpr (KV) LR::template ce_kv<b>(v, w);
+      else LR::template ce<b>(v);
     }
   }
 
   template <int r, int I>
-  __device__ __forceinline__ static void steps(const Ctx& c, uint32_t (&v)[NR]) {
+  __device__ __forceinline__ static void steps(const Ctx& c, uint32_t (&v)[NR],
+                                               uint32_t (&w)[NR]) {
     if constexpr (I < RD::begin(r + 1)) {
       if constexpr (I > 0 && S::phase(I) != S::phase(I - 1)) {
         transition<L<r>, S::phase(I - 1), S::phase(I)>(c, v, 0u);
       }
-      one_step<L<r>, I>(v);
-      steps<r, I + 1>(c, v);
+      one_step<L<r>, I>(v, w);
+      steps<r, I + 1>(c, v, w);
     }
   }
 
@@ -397,66 +397,91 @@ struct PassBody {
     }
   }
 
-  // Keys -> registers in round 0's layout (phase domain of the first step).
-  __device__ __forceinline__ static void load(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR]) {
+  // shared-memory words of one tile array (keys; payloads follow when KV)
+  static constexpr uint32_t TW = (uint32_t)tile_smem_words(C);
+
+  // Keys (and payloads) -> registers in round 0's layout (phase domain of
+  // the first step).
+  __device__ __forceinline__ static void load(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR],
+                                              uint32_t (&w)[NR]) {
     using L0 = L<0>;
     constexpr int PH = S::phase(0);
     if constexpr (direct_ok<L0>()) {
       const uint32_t tj = L0::thread_j();
       gload<L0>(c, tj, v);
+      if constexpr (KV) {
+        Ctx cv = c;
+        cv.keys = c.vals;
+        gload<L0>(cv, tj, w);
+      }
       apply_mask<L0, PH, -1, true>(c, v, c.gin);
     } else {
       constexpr int db = natural(PH) ? -1 : dloc(PH);
       const uint32_t u = (natural(PH) || db >= 0) ? 0u : uni(c, PH);
       stage_in<C, A, db, R>(sm, c.keys, c.gbase, c.y, c.gin ^ u);
+      if constexpr (KV) stage_in<C, A, -1, R>(sm + TW, c.vals, c.gbase, c.y, 0u);
       L0::lds(sm, v);
+      if constexpr (KV) L0::lds(sm + TW, w);
     }
   }
 
-  // Registers (last round's layout, last phase's domain) -> keys.
-  __device__ __forceinline__ static void store(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR]) {
+  // Registers (last round's layout, last phase's domain) -> keys (+ payloads).
+  __device__ __forceinline__ static void store(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR],
+                                               uint32_t (&w)[NR]) {
     using LL = L<NRND - 1>;
     constexpr int PH = S::phase(S::len() - 1);
     const uint32_t tj = LL::thread_j();
     apply_mask<LL, PH, -1, true>(c, v, c.gout);
     if constexpr (direct_ok<LL>()) {
       gstore<LL>(c, tj, v);
+      if constexpr (KV) {
+        Ctx cv = c;
+        cv.keys = c.vals;
+        gstore<LL>(cv, tj, w);
+      }
     } else {
       LL::sts(sm, v);
+      if constexpr (KV) LL::sts(sm + TW, w);
       stage_out<C, A, R>(sm, c.keys, c.gbase, c.y);
+      if constexpr (KV) stage_out<C, A, R>(sm + TW, c.vals, c.gbase, c.y);
     }
   }
 
   template <int r>
-  __device__ __forceinline__ static void rounds(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR]) {
+  __device__ __forceinline__ static void rounds(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR],
+                                                uint32_t (&w)[NR]) {
     if constexpr (r < NRND) {
       if constexpr (r > 0) {
         L<r - 1>::sts(sm, v);
+        if constexpr (KV) L<r - 1>::sts(sm + TW, w);
         __syncthreads();
         L<r>::lds(sm, v);
+        if constexpr (KV) L<r>::lds(sm + TW, w);
       }
-      steps<r, RD::begin(r)>(c, v);
-      rounds<r + 1>(c, sm, v);
+      steps<r, RD::begin(r)>(c, v, w);
+      rounds<r + 1>(c, sm, v, w);
     }
   }
 
   __device__ __forceinline__ static void run(const Ctx& c, uint32_t* sm) {
     uint32_t v[NR];
+    uint32_t w[NR];  // payload registers (dead code unless KV)
     pdl_wait();
-    load(c, sm, v);
-    rounds<0>(c, sm, v);
-    store(c, sm, v);
+    load(c, sm, v, w);
+    rounds<0>(c, sm, v, w);
+    store(c, sm, v, w);
     pdl_trigger();
   }
 };
 
-template <int C, int R = reg_bits(C)>
+template <int C, int R = reg_bits(C), bool KV = false>
 __global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
 tile_sort_kernel(PassParams P) {
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 0, -1, -1, R>;
+  using B = PassBody<C, 0, -1, -1, R, KV>;
   typename B::Ctx c;
   c.keys = P.keys;
+  c.vals = P.vals;
   c.gbase = (uint64_t)blockIdx.x << C;
   c.y = C;
   c.uA = c.uB = 0u;
@@ -466,15 +491,16 @@ tile_sort_kernel(PassParams P) {
   B::run(c, smem);
 }
 
-template <int C, int SA, int SB, int R = reg_bits(C)>
+template <int C, int SA, int SB, int R = reg_bits(C), bool KV = false>
 __global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
 merge_kernel(PassParams P) {
   static_assert(SA >= 0 || SB >= 0, "empty pass");
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 1, SA, SB, R>;
+  using B = PassBody<C, 1, SA, SB, R, KV>;
   constexpr int A = B::A;
   typename B::Ctx c;
   c.keys = P.keys;
+  c.vals = P.vals;
   c.y = P.y;
   c.gbase = Coset<C, A>::base(blockIdx.x, P.y);
   c.uA = 0u - dir_bit_global(c.gbase, P.pA, P.kd);

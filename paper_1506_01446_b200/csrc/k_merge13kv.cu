@@ -1,0 +1,3 @@
+// key-value merge kernels, 13-bit tiles, 16 pairs per thread
+#include "merge_table.cuh"
+B200_DEFINE_MERGE_TABLE_KV(13)

@@ -9,11 +9,11 @@ using PassFn = void (*)(PassParams);
 
 // Tile-sort kernel for a 2^C tile (C in [1, 15]) with 2^R keys per thread
 // (R = 5, or R = 4 for the instantiated latency-bound sizes).
-PassFn find_tile_kernel(int C, int R = 5);
+PassFn find_tile_kernel(int C, int R = 5, bool kv = false);
 // Specialised merge kernel for local bits SA..0 then C-1..SB, or nullptr when
 // that shape was not instantiated (the caller then uses the runtime-dispatched
 // bitonic_pass_kernel<C>).
-PassFn find_merge_kernel(int C, int SA, int SB, int R = 5);
+PassFn find_merge_kernel(int C, int SA, int SB, int R = 5, bool kv = false);
 
 // Instantiated merge tile sizes.
 constexpr int kMergeCMin = 11;
@@ -32,5 +32,7 @@ void fill_merge_table_14(MergeTable& t);
 void fill_merge_table_15(MergeTable& t);
 void fill_merge_table_12_r4(MergeTable& t);
 void fill_merge_table_13_r4(MergeTable& t);
+void fill_merge_table_12_kv(MergeTable& t);
+void fill_merge_table_13_kv(MergeTable& t);
 
 }  // namespace b200

@@ -8,26 +8,26 @@
 
 namespace b200 {
 
-template <int C, int A, int R>
+template <int C, int A, int R, bool KV>
 PassFn th_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A, R>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A, R, KV>;
   else return nullptr;
 }
-template <int C, int A, int R>
+template <int C, int A, int R, bool KV>
 PassFn ho_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A, R>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A, R, KV>;
   else return nullptr;
 }
-template <int C, int SA, int R>
+template <int C, int SA, int R, bool KV>
 PassFn to_entry() {
-  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1, R>;
+  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1, R, KV>;
   else return nullptr;
 }
-template <int C, int R, int... I>
+template <int C, int R, bool KV, int... I>
 void fill_merge_table(MergeTable& t, std::integer_sequence<int, I...>) {
-  ((t.th[I] = th_entry<C, I, R>()), ...);
-  ((t.ho[I] = ho_entry<C, I, R>()), ...);
-  ((t.to[I] = to_entry<C, I, R>()), ...);
+  ((t.th[I] = th_entry<C, I, R, KV>()), ...);
+  ((t.ho[I] = ho_entry<C, I, R, KV>()), ...);
+  ((t.to[I] = to_entry<C, I, R, KV>()), ...);
 }
 
 }  // namespace b200
@@ -35,13 +35,20 @@ void fill_merge_table(MergeTable& t, std::integer_sequence<int, I...>) {
 #define B200_DEFINE_MERGE_TABLE(CC)                                      \
   namespace b200 {                                                       \
   void fill_merge_table_##CC(MergeTable& t) {                            \
-    fill_merge_table<CC, 5>(t, std::make_integer_sequence<int, 16>{});   \
+    fill_merge_table<CC, 5, false>(t, std::make_integer_sequence<int, 16>{}); \
   }                                                                      \
   }
 
 #define B200_DEFINE_MERGE_TABLE_R4(CC)                                   \
   namespace b200 {                                                       \
   void fill_merge_table_##CC##_r4(MergeTable& t) {                       \
-    fill_merge_table<CC, 4>(t, std::make_integer_sequence<int, 16>{});   \
+    fill_merge_table<CC, 4, false>(t, std::make_integer_sequence<int, 16>{}); \
+  }                                                                      \
+  }
+
+#define B200_DEFINE_MERGE_TABLE_KV(CC)                                   \
+  namespace b200 {                                                       \
+  void fill_merge_table_##CC##_kv(MergeTable& t) {                       \
+    fill_merge_table<CC, 4, true>(t, std::make_integer_sequence<int, 16>{}); \
   }                                                                      \
   }

@@ -129,6 +129,7 @@ struct PlanOptions {
   int cmin = 6;    // ... but not below this tile size
   int regbits = 0; // keys per thread = 2^regbits (0 = automatic)
   bool dp = true;  // cost-model planner (false: greedy packing)
+  bool kv = false; // key-value plan: 16 pairs per thread, 2^12 / 2^13 tiles
   double trip_cost = 0.10;  // extra cost of a shared-memory round trip, in passes
 };
 
@@ -179,6 +180,12 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     while (C > k && C > opt.cmin && (total >> C) < (uint64_t)opt.min_ctas) --C;
   }
   if (C > kt) C = kt;
+  if (opt.kv) {
+    // key-value kernels exist for tiles up to 2^13 and merges on 2^12 / 2^13
+    if (C > 13) C = 13;
+    if (k > C && C < 12) C = 12;
+    if (C > kt) C = kt;
+  }
   // Merge passes need a coalescing run below the high range and a phase
   // direction bit that is per-thread uniform in layout L_0 (C - 1 >= 5).
   if (k > C && C < opt.lrun + 1) C = opt.lrun + 1;
@@ -200,6 +207,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // (measured on B200).
   int R = opt.regbits > 0 ? opt.regbits
                           : ((k <= 19 && batch == 1) || (batch > 1 && C >= 10 && C <= 14) ? 4 : 5);
+  if (opt.kv) R = C < 4 ? C : 4;
   for (auto& q : plan) q.R = R;
   if (k <= C) return plan;
 
@@ -237,7 +245,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     plan.push_back(m);
   };
 
-  if (opt.dp) {
+  if (opt.dp || opt.kv) {
     // Dynamic program over (phase p, next step bit b): each pass costs 1 plus
     // trip_cost per extra shared-memory round trip; shapes are restricted to
     // the instantiated kernel families (tail-only, tail+head with a = b+1,

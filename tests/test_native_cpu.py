@@ -205,3 +205,9 @@ def test_no_cpu_fallback():
         b200.sort_(torch.arange(16, dtype=torch.int32))
     with pytest.raises(b200.InvalidSizeError):
         b200.sequential_bitonic_sort(np.zeros(6, np.int32))
+
+
+def test_key_value_entry_validates():
+    L = _native.lib()
+    assert L.b200_bitonic_sort_pairs_u32(None, None, 16, 0, None) == 2
+    assert L.b200_bitonic_sort_pairs_u32(None, None, 6, 0, None) in (1, 2)
