@@ -57,6 +57,7 @@ b200::PlanOptions plan_options() {
   o.lrun = g_min_run_bits.load();
   if (const char* e = std::getenv("B200_BITONIC_REGBITS")) o.regbits = std::atoi(e);
   if (const char* e = std::getenv("B200_BITONIC_PLANNER")) o.dp = std::strcmp(e, "greedy") != 0;
+  if (const char* e = std::getenv("B200_BITONIC_TILE_REGBITS")) o.tile_regbits = std::atoi(e);
   return o;
 }
 
@@ -173,18 +174,19 @@ std::mutex g_plan_mu;
 struct PlanKey {
   int k;
   uint64_t batch;
-  int cmax, cmin, lrun, min_ctas, regbits;
+  int cmax, cmin, lrun, min_ctas, regbits, tile_regbits;
   bool dp, kv;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
            lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp &&
-           kv == o.kv;
+           kv == o.kv && tile_regbits == o.tile_regbits;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
-  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.dp, o.kv};
+  const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.tile_regbits,
+                    o.dp, o.kv};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;

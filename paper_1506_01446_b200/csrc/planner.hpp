@@ -128,6 +128,7 @@ struct PlanOptions {
   int min_ctas = 128;  // shrink the tile until the grid has this many CTAs
   int cmin = 6;    // ... but not below this tile size
   int regbits = 0; // keys per thread = 2^regbits (0 = automatic)
+  int tile_regbits = 0;  // override for the tile-sort pass only (0 = same)
   bool dp = true;  // cost-model planner (false: greedy packing)
   bool kv = false; // key-value plan: 16 pairs per thread, 2^12 / 2^13 tiles
   double trip_cost = 0.10;  // extra cost of a shared-memory round trip, in passes
@@ -209,6 +210,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
                           : ((k <= 19 && batch == 1) || (batch > 1 && C >= 10 && C <= 14) ? 4 : 5);
   if (opt.kv) R = C < 4 ? C : 4;
   for (auto& q : plan) q.R = R;
+  if (opt.tile_regbits > 0 && !opt.kv) plan.front().R = opt.tile_regbits;
   if (k <= C) return plan;
 
   const int lrun = opt.lrun;
