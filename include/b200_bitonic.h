@@ -94,6 +94,29 @@ int b200_bitonic_sort_pairs_u32_batched(uint32_t* d_keys, uint32_t* d_vals,
 int b200_bitonic_sort_f32(float* d_keys, uint64_t n, int descending,
                           b200_stream_t stream);
 
+/* 64-bit keys (the paper's other future-work key types, PAPER.md:125:
+ * 64-bit integers and doubles).  The network runs on two word planes (hi,
+ * lo) compared lexicographically, 16 keys per thread; the interleaved entry
+ * points split the array into a stream-ordered scratch pair of planes, sort
+ * and join back (float64: IEEE totalOrder like b200_bitonic_sort_f32).
+ * b200_bitonic_sort_u64_planes sorts keys already held as planes
+ * (key i = hi[i] << 32 | lo[i]) in place with no scratch.  n must be a
+ * power of two >= 2; pointers 16-byte aligned. */
+int b200_bitonic_sort_u64(uint64_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream);
+int b200_bitonic_sort_i64(int64_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream);
+int b200_bitonic_sort_f64(double* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream);
+int b200_bitonic_sort_u64_planes(uint32_t* d_hi, uint32_t* d_lo, uint64_t n,
+                                 int descending, b200_stream_t stream);
+
+/* Scratch buffers (padded copies, 64-bit word planes, merge coranks, host
+ * staging) come from a library-owned stream-ordered pool per device that
+ * retains freed memory for the next call; this returns it to the driver.
+ * Call only when no sort is in flight. */
+int b200_bitonic_release_scratch(void);
+
 /* Any length n >= 1 (the reference's pad_to_pow2 + sort + truncate,
  * bench.cpp:366-377, acceptance.cpp:114-156): when n is not a power of two
  * the keys are copied into a stream-ordered scratch buffer of bit_ceil(n)

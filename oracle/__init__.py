@@ -57,6 +57,8 @@ class Oracle:
                                                    ctypes.c_uint64, ctypes.c_int]
         lib.oracle_bitonic_pairs.argtypes = [_u32p, _u32p, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.c_uint32]
+        lib.oracle_bitonic_u64.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int,
+                                           ctypes.c_uint64]
         lib.oracle_quicksort_i32.argtypes = [_i32p, ctypes.c_uint64]
         lib.oracle_quicksort_i32.restype = None
         lib.oracle_quicksort_u32.argtypes = [_u32p, ctypes.c_uint64, ctypes.c_int]
@@ -108,6 +110,27 @@ class Oracle:
                                          int(descending), kx):
             raise ValueError("length must be a power of two >= 2")
         return k.view(keys.dtype), v
+
+    def bitonic_64(self, keys: np.ndarray, descending: bool = False) -> np.ndarray:
+        """The reference network on int64 / uint64 / float64 keys (float64 in
+        IEEE totalOrder, -NaN < -inf < ... < -0.0 < +0.0 < ... < +NaN)."""
+        dt = keys.dtype
+        a = np.ascontiguousarray(keys).view(np.uint64).copy()
+        kx = 0
+        if dt == np.int64:
+            kx = 1 << 63
+        elif dt == np.float64:
+            neg = (a >> np.uint64(63)).astype(bool)
+            a = np.where(neg, ~a, a | np.uint64(1 << 63))
+        elif dt != np.uint64:
+            raise TypeError(f"64-bit keys expected, got {dt}")
+        a = np.ascontiguousarray(a)
+        if self.lib.oracle_bitonic_u64(a.ctypes.data, a.size, int(descending), kx):
+            raise ValueError("length must be a power of two >= 2")
+        if dt == np.float64:
+            neg = ~(a >> np.uint64(63)).astype(bool)
+            a = np.where(neg, ~a, a & np.uint64((1 << 63) - 1))
+        return np.ascontiguousarray(a).view(dt)
 
     def quicksort_i32(self, keys: np.ndarray) -> np.ndarray:
         a = np.ascontiguousarray(keys, dtype=np.int32).copy()

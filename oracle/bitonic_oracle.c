@@ -23,6 +23,7 @@
  *                             compare_exchange :16-22)
  *   oracle_bitonic_u32        same network, uint32 order, with the new
  *                             `descending` argument north_star asks for
+ *   oracle_bitonic_u64        same network on 64-bit keys (int64 via key_xor)
  *   oracle_quicksort_i32      proj/src/verify.cpp:17-75, :109-116
  *   oracle_predicted_counts   proj/src/schedule.cpp:71-78
  *   oracle_fnv1a64            digest used for the golden fixtures (SURVEY.md
@@ -180,6 +181,34 @@ int oracle_bitonic_pairs(uint32_t* k, uint32_t* v, uint64_t n, int descending,
           uint32_t tv = v[i];
           v[i] = v[i + stride];
           v[i + stride] = tv;
+        }
+      }
+    }
+  }
+  return ORACLE_OK;
+}
+
+/* 64-bit keys (the paper's future-work types): the same
+ * network (engine.cpp:248-266) on uint64 keys compared after XOR with
+ * key_xor (1 << 63 = int64 order).  float64 order is the caller's totalOrder
+ * bit map (oracle/__init__.py) onto this uint64 order. */
+int oracle_bitonic_u64(uint64_t* a, uint64_t n, int descending, uint64_t key_xor) {
+  if (!is_pow2_ge2(n)) return ORACLE_INVALID_SIZE;
+  unsigned k = 0;
+  while ((1ULL << k) < n) ++k;
+  for (unsigned phase = 1; phase <= k; ++phase) {
+    const uint64_t span = 1ULL << phase;
+    for (unsigned step = phase; step >= 1; --step) {
+      const uint64_t stride = 1ULL << (step - 1);
+      for (uint64_t t = 0; t < n / 2; ++t) {
+        const uint64_t i = pair_base(t, stride);
+        int asc = (i & span) == 0;
+        if (descending) asc = !asc;
+        const uint64_t x = a[i] ^ key_xor, y = a[i + stride] ^ key_xor;
+        if (asc ? (x > y) : (x < y)) {
+          const uint64_t tk = a[i];
+          a[i] = a[i + stride];
+          a[i + stride] = tk;
         }
       }
     }

@@ -34,9 +34,9 @@ from . import _native
 
 __all__ = [
     "InvalidSizeError", "ConfigError", "CudaError",
-    "sort_", "sort_pairs_", "argsort", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
+    "sort_", "sort_pairs_", "sort_planes_", "argsort", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
     "merge_split_", "merge_", "sort_multi", "plan", "counters", "set_tuning",
-    "PassPlan", "version", "library_path",
+    "PassPlan", "version", "library_path", "release_scratch",
 ]
 
 
@@ -88,7 +88,21 @@ def _key_dtype(t):
         return "u32"
     if t.dtype == torch.float32:
         return "f32"
-    raise ConfigError(f"keys must be int32, uint32 or float32, got {t.dtype}")
+    if t.dtype == torch.int64:
+        return "i64"
+    if t.dtype == torch.uint64:
+        return "u64"
+    if t.dtype == torch.float64:
+        return "f64"
+    raise ConfigError(f"keys must be int32, uint32, float32, int64, uint64 or float64, "
+                      f"got {t.dtype}")
+
+
+def _key_dtype32(t):
+    kind = _key_dtype(t)
+    if kind not in ("i32", "u32"):
+        raise ConfigError(f"this entry point takes int32 or uint32 keys, got {t.dtype}")
+    return kind
 
 
 def _check_tensor(t) -> None:
@@ -100,12 +114,14 @@ def _check_tensor(t) -> None:
 
 def sort_(t, descending: bool = False, stream=None):
     """Sort a 1-D CUDA tensor of int32 (signed order, the reference's key type),
-    uint32, or float32 (IEEE totalOrder) keys in place; asynchronous on
-    ``stream`` (default: current)."""
+    uint32, float32 (IEEE totalOrder), int64, uint64 or float64 keys in place;
+    asynchronous on ``stream`` (default: current)."""
     _check_tensor(t)
     kind = _key_dtype(t)
-    fn = {"i32": _native.lib().b200_bitonic_sort_i32, "u32": _native.lib().b200_bitonic_sort_u32,
-          "f32": _native.lib().b200_bitonic_sort_f32}[kind]
+    L = _native.lib()
+    fn = {"i32": L.b200_bitonic_sort_i32, "u32": L.b200_bitonic_sort_u32,
+          "f32": L.b200_bitonic_sort_f32, "i64": L.b200_bitonic_sort_i64,
+          "u64": L.b200_bitonic_sort_u64, "f64": L.b200_bitonic_sort_f64}[kind]
     _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
               ctypes.c_void_p(_stream_ptr(stream))))
     return t
@@ -121,14 +137,30 @@ def sort_pairs_(keys, values, descending: bool = False, stream=None):
     _check_tensor(values)
     if values.numel() != keys.numel() or values.element_size() != 4:
         raise ConfigError("values must be a 32-bit tensor with one entry per key")
-    kind = _key_dtype(keys)
-    if kind == "f32":
-        raise ConfigError("key-value sort takes int32 or uint32 keys")
+    kind = _key_dtype32(keys)
     fn = (_native.lib().b200_bitonic_sort_pairs_i32 if kind == "i32"
           else _native.lib().b200_bitonic_sort_pairs_u32)
     _check(fn(ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
               keys.numel(), int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
     return keys, values
+
+
+def sort_planes_(hi, lo, descending: bool = False, stream=None):
+    """64-bit keys held as two uint32/int32 word planes (key i = hi[i] << 32 |
+    lo[i], unsigned), sorted in place with no scratch memory."""
+    _check_tensor(hi)
+    _check_tensor(lo)
+    if hi.element_size() != 4 or lo.element_size() != 4 or hi.numel() != lo.numel():
+        raise ConfigError("hi and lo must be 32-bit tensors of equal length")
+    _check(_native.lib().b200_bitonic_sort_u64_planes(
+        ctypes.c_void_p(hi.data_ptr()), ctypes.c_void_p(lo.data_ptr()), hi.numel(),
+        int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
+    return hi, lo
+
+
+def release_scratch() -> None:
+    """Return the library's retained scratch memory (all devices) to the driver."""
+    _check(_native.lib().b200_bitonic_release_scratch())
 
 
 def argsort(keys, descending: bool = False, stream=None):
@@ -145,9 +177,7 @@ def sort_padded_(t, descending: bool = False, stream=None):
     (bench.cpp:366-377) -- non-powers of two go through a padded scratch
     buffer (stream-ordered allocation); powers of two sort in place."""
     _check_tensor(t)
-    kind = _key_dtype(t)
-    if kind == "f32":
-        raise ConfigError("float32 keys: use sort_")
+    kind = _key_dtype32(t)
     fn = (_native.lib().b200_bitonic_sort_padded_i32 if kind == "i32"
           else _native.lib().b200_bitonic_sort_padded_u32)
     _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
@@ -160,9 +190,7 @@ def sort_batched_(t, n_per_array: int, descending: bool = False, stream=None):
     _check_tensor(t)
     if n_per_array < 1 or t.numel() % n_per_array:
         raise ConfigError("numel must be a multiple of n_per_array")
-    kind = _key_dtype(t)
-    if kind == "f32":
-        raise ConfigError("float32 keys: use sort_")
+    kind = _key_dtype32(t)
     fn = (_native.lib().b200_bitonic_sort_i32_batched if kind == "i32"
           else _native.lib().b200_bitonic_sort_u32_batched)
     _check(fn(ctypes.c_void_p(t.data_ptr()), n_per_array, t.numel() // n_per_array,

@@ -23,6 +23,11 @@ EXPORTED = (
     "b200_bitonic_sort_pairs_i32",
     "b200_bitonic_sort_pairs_u32_batched",
     "b200_bitonic_sort_f32",
+    "b200_bitonic_sort_u64",
+    "b200_bitonic_sort_i64",
+    "b200_bitonic_sort_f64",
+    "b200_bitonic_sort_u64_planes",
+    "b200_bitonic_release_scratch",
     "b200_bitonic_sort_padded_u32",
     "b200_bitonic_sort_padded_i32",
     "b200_bitonic_sort_host_i32",

@@ -69,6 +69,8 @@ struct PassParams {
   uint32_t* vals;     // payloads moved with the keys (key-value kernels only)
   uint32_t gmask_in;  // XOR applied at load  (key order transform, first pass)
   uint32_t gmask_out; // XOR applied at store (inverse transform, last pass)
+  uint32_t gmask_in_lo;   // low-word transforms of 64-bit keys
+  uint32_t gmask_out_lo;
   int a;              // local bits [0,a) -> global bits [0,a)
   int y;              // local bits [a,C) -> global bits [y, y+C-a)
   int kd;             // log2 of one sorted array: phase kd has no direction bit

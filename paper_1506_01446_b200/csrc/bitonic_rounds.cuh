@@ -365,6 +365,52 @@ struct Layout {
       }
     }
   }
+  // 64-bit keys held as (hi word in v, lo word in w): lexicographic CE,
+  // swap only when strictly out of order.
+  template <int B>
+  __device__ __forceinline__ static void ce_k64(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+    constexpr int q = qof(B);
+    static_assert(q >= 0, "CE bit must be a register bit");
+#pragma unroll
+    for (int e = 0; e < NR; ++e) {
+      if (!(e & (1 << q))) {
+        const int f = e | (1 << q);
+        // x > y implies hi(x) >= hi(y): the high words are a plain min/max,
+        // only the low words follow the 64-bit predicate.
+        const uint64_t x = ((uint64_t)v[e] << 32) | w[e];
+        const uint64_t y = ((uint64_t)v[f] << 32) | w[f];
+        const bool sw = x > y;
+        const uint32_t a = w[e], b = w[f];
+        const uint32_t h0 = min(v[e], v[f]), h1 = max(v[e], v[f]);
+        v[e] = h0;
+        v[f] = h1;
+        w[e] = sw ? b : a;
+        w[f] = sw ? a : b;
+      }
+    }
+  }
+  template <int B, int D>
+  __device__ __forceinline__ static void ce_dir_k64(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+    constexpr int q = qof(B);
+    constexpr int qd = qof(D);
+    static_assert(q >= 0 && qd >= 0, "CE and direction bits must be register bits");
+#pragma unroll
+    for (int e = 0; e < NR; ++e) {
+      if (!(e & (1 << q))) {
+        const int f = e | (1 << q);
+        const uint64_t x = ((uint64_t)v[e] << 32) | w[e];
+        const uint64_t y = ((uint64_t)v[f] << 32) | w[f];
+        const bool desc = (e >> qd) & 1;
+        const bool sw = desc ? (x < y) : (x > y);
+        const uint32_t a = w[e], b = w[f];
+        const uint32_t h0 = min(v[e], v[f]), h1 = max(v[e], v[f]);
+        v[e] = desc ? h1 : h0;
+        v[f] = desc ? h0 : h1;
+        w[e] = sw ? b : a;
+        w[f] = sw ? a : b;
+      }
+    }
+  }
   // XOR register e with all-ones when bit LB of its local index is set
   // (LB a register bit) -- or with the per-thread uniform u when LB is a
   // thread bit -- or with u when LB < 0 (uniform source).

@@ -98,17 +98,53 @@ b200::PassFn generic_kernel(int C) {
   }
 }
 
+// Scratch memory (padded copies, 64-bit word planes, merge coranks, host
+// staging) comes from one library-owned stream-ordered pool per device that
+// keeps freed memory (release threshold = max): after the first call of a
+// given size, allocation is a pool lookup instead of a fresh mapping.
+std::mutex g_pool_mu;
+std::vector<cudaMemPool_t> g_pools;
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1, nullptr);
+    if (g_pools[dev] == nullptr) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&g_pools[dev], &props);
+      if (e != cudaSuccess) return e;
+      uint64_t keep = ~uint64_t{0};
+      cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool = g_pools[dev];
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+template <class T>
+cudaError_t scratch_alloc(T** p, size_t bytes, cudaStream_t s) {
+  return scratch_alloc(reinterpret_cast<void**>(p), bytes, s);
+}
+
 std::atomic<int> g_force_generic{0};
 std::atomic<int> g_pdl{1};  // programmatic dependent launch between passes
 
 // Returns the kernel and its keys-per-thread exponent (the block size is
 // 2^(C - R)).  Shapes without a 16-keys-per-thread instantiation fall back to
 // 32 keys per thread.
-b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out, bool kv) {
-  if (kv) {
+// mode: 0 keys, 1 key + payload, 2 64-bit keys (two word arrays).
+b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out, int mode) {
+  if (mode != 0) {
     *R_out = q.R;
-    return q.tile_sort ? (q.p_end == q.C ? b200::find_tile_kernel(q.C, q.R, true) : nullptr)
-                       : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo, q.R, true);
+    return q.tile_sort ? (q.p_end == q.C ? b200::find_tile_kernel(q.C, q.R, mode) : nullptr)
+                       : b200::find_merge_kernel(q.C, q.segA_hi, q.segB_lo, q.R, mode);
   }
   if (!g_force_generic.load()) {
     for (int R : {q.R, 5}) {
@@ -144,11 +180,11 @@ cudaError_t ensure_attr(const void* fn, int C, int arrays) {
   return e;
 }
 
-cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p,
-                        cudaStream_t s) {
+cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p, cudaStream_t s,
+                        int mode) {
   int R = 5;
-  const bool kv = p.vals != nullptr;
-  b200::PassFn f = select_kernel(q, &R, kv);
+  const bool kv = mode != 0;
+  b200::PassFn f = select_kernel(q, &R, mode);
   if (f == nullptr) return cudaErrorNotSupported;  // no such key-value shape
   const void* fn = reinterpret_cast<const void*>(f);
   cudaError_t e = ensure_attr(fn, q.C, kv ? 2 : 1);
@@ -197,10 +233,14 @@ std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanO
 }
 
 // Validates and runs the whole plan (or only pass `only`, when >= 0).
-// key_xor: 0x80000000 for int32 keys.
+// key_xor: 0x80000000 for int32 keys (for 64-bit keys: applied to the hi
+// word).  d_vals: payloads (mode 1) or the lo words of 64-bit keys whose hi
+// words are d_keys (mode 2).
 int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
               uint32_t key_xor, cudaStream_t stream, int only = -1,
-              uint32_t* d_vals = nullptr) {
+              uint32_t* d_vals = nullptr, int mode = -1) {
+  if (mode < 0) mode = d_vals != nullptr ? 1 : 0;
+  if (mode != 0 && d_vals == nullptr) return fail(B200_CONFIG, "null second array");
   if (n_per < 2 || !is_pow2(n_per)) {
     return fail(B200_INVALID_SIZE,
                 "length must be a power of two >= 2, got " +
@@ -228,6 +268,7 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     return fail(B200_CONFIG, "device pointers must be 16-byte aligned");
   }
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+  const uint32_t gmask_lo = (mode == 2 && descending) ? 0xFFFFFFFFu : 0u;
   if (only >= (int)plan.size()) return fail(B200_CONFIG, "pass index outside the plan");
   for (size_t i = 0; i < plan.size(); ++i) {
     if (only >= 0 && (int)i != only) continue;
@@ -237,6 +278,8 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     p.vals = d_vals;
     p.gmask_in = (i == 0) ? gmask : 0u;
     p.gmask_out = (i + 1 == plan.size()) ? gmask : 0u;
+    p.gmask_in_lo = (i == 0) ? gmask_lo : 0u;
+    p.gmask_out_lo = (i + 1 == plan.size()) ? gmask_lo : 0u;
     p.a = q.a;
     p.y = q.y;
     p.kd = k;
@@ -246,7 +289,7 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     p.pA = q.pA;
     p.segB_lo = q.segB_lo;
     p.pB = q.pB;
-    cudaError_t e = launch_pass(q, p, stream);
+    cudaError_t e = launch_pass(q, p, stream, mode);
     if (e == cudaErrorNotSupported) {
       return fail(B200_CONFIG, "no key-value kernel for this tile size (use tile_bits 0, 12 or 13)");
     }
@@ -292,6 +335,54 @@ __global__ void f32_to_key_kernel(uint32_t* d, uint64_t n, int inverse) {
   }
 }
 
+// 64-bit keys <-> (hi, lo) word planes.  kind 2 (float64) applies the
+// totalOrder bit map x ^ (sign ? ~0 : 1 << 63) on the way in, undoes it on
+// the way out.
+__global__ void split64_kernel(const uint64_t* __restrict__ src, uint32_t* __restrict__ hi,
+                               uint32_t* __restrict__ lo, uint64_t n, int kind) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t x = src[i];
+    if (kind == 2) x ^= (uint64_t)((int64_t)x >> 63) | 0x8000000000000000ull;
+    hi[i] = (uint32_t)(x >> 32);
+    lo[i] = (uint32_t)x;
+  }
+}
+
+__global__ void join64_kernel(uint64_t* __restrict__ dst, const uint32_t* __restrict__ hi,
+                              const uint32_t* __restrict__ lo, uint64_t n, int kind) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t x = ((uint64_t)hi[i] << 32) | lo[i];
+    if (kind == 2) x ^= (uint64_t)((int64_t)~x >> 63) | 0x8000000000000000ull;
+    dst[i] = x;
+  }
+}
+
+// kind: 0 uint64, 1 int64, 2 float64
+int sort64_impl(uint64_t* d_keys, uint64_t n, int descending, int kind, cudaStream_t s) {
+  if (n < 2 || !is_pow2(n)) {
+    return fail(B200_INVALID_SIZE,
+                "length must be a power of two >= 2, got " + std::to_string(n));
+  }
+  if (d_keys == nullptr) return fail(B200_CONFIG, "null key pointer");
+  if (descending != 0 && descending != 1) {
+    return fail(B200_CONFIG, "descending must be 0 or 1");
+  }
+  uint32_t* planes = nullptr;
+  B200_CUDA_TRY(scratch_alloc(&planes, n * 8, s));
+  uint32_t* hi = planes;
+  uint32_t* lo = planes + n;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  split64_kernel<<<grid, 256, 0, s>>>(d_keys, hi, lo, n, kind);
+  int rc = sort_impl(hi, n, 1, descending, kind == 1 ? 0x80000000u : 0u, s, -1, lo, 2);
+  if (rc == B200_OK) join64_kernel<<<grid, 256, 0, s>>>(d_keys, hi, lo, n, kind);
+  cudaFreeAsync(planes, s);
+  cudaError_t e = cudaGetLastError();
+  if (rc == B200_OK && e != cudaSuccess) rc = cuda_fail(e, "64-bit key transform");
+  return rc;
+}
+
 __global__ void pad_fill_kernel(uint32_t* dst, const uint32_t* src, uint64_t n,
                                 uint64_t m, uint32_t pad) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -317,7 +408,7 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
   const uint32_t pad = ~gmask;
   uint32_t* tmp = nullptr;
-  B200_CUDA_TRY(cudaMallocAsync(&tmp, m * 4, s));
+  B200_CUDA_TRY(scratch_alloc(&tmp, m * 4, s));
   const unsigned grid = (unsigned)std::min<uint64_t>((m + 255) / 256, 148 * 8);
   pad_fill_kernel<<<grid, 256, 0, s>>>(tmp, d_keys, n, m, pad);
   int rc = sort_impl(tmp, m, 1, descending, key_xor, s);
@@ -377,6 +468,40 @@ int b200_bitonic_sort_f32(float* d_keys, uint64_t n, int descending,
   return rc;
 }
 
+int b200_bitonic_sort_u64(uint64_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream) {
+  return sort64_impl(d_keys, n, descending, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_i64(int64_t* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream) {
+  return sort64_impl(reinterpret_cast<uint64_t*>(d_keys), n, descending, 1,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_f64(double* d_keys, uint64_t n, int descending,
+                          b200_stream_t stream) {
+  return sort64_impl(reinterpret_cast<uint64_t*>(d_keys), n, descending, 2,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_u64_planes(uint32_t* d_hi, uint32_t* d_lo, uint64_t n,
+                                 int descending, b200_stream_t stream) {
+  if (d_lo == nullptr) return fail(B200_CONFIG, "null low-word pointer");
+  return sort_impl(d_hi, n, 1, descending, 0u, reinterpret_cast<cudaStream_t>(stream), -1,
+                   d_lo, 2);
+}
+
+int b200_bitonic_release_scratch(void) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (cudaMemPool_t p : g_pools) {
+    if (p == nullptr) continue;
+    cudaError_t e = cudaMemPoolTrimTo(p, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "trim scratch pool");
+  }
+  return B200_OK;
+}
+
 int b200_bitonic_sort_padded_u32(uint32_t* d_keys, uint64_t n, int descending,
                                  b200_stream_t stream) {
   return padded_impl(d_keys, n, descending, 0u, reinterpret_cast<cudaStream_t>(stream));
@@ -424,10 +549,10 @@ static int host_sort(uint32_t* h, uint64_t n, int descending, uint32_t key_xor) 
   uint32_t* d = nullptr;
   cudaStream_t s = nullptr;
   B200_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  cudaError_t e = cudaMallocAsync(&d, n * 4, s);
+  cudaError_t e = scratch_alloc(&d, n * 4, s);
   if (e != cudaSuccess) {
     cudaStreamDestroy(s);
-    return cuda_fail(e, "cudaMallocAsync");
+    return cuda_fail(e, "scratch allocation");
   }
   int rc = B200_OK;
   e = cudaMemcpyAsync(d, h, n * 4, cudaMemcpyHostToDevice, s);
@@ -464,7 +589,7 @@ int b200_bitonic_merge_u32(const uint32_t* a, uint64_t la, const uint32_t* b,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const uint64_t tiles = (la + lb + b200::kMergeTile - 1) / b200::kMergeTile;
   uint64_t* cor = nullptr;
-  B200_CUDA_TRY(cudaMallocAsync(&cor, (tiles + 1) * sizeof(uint64_t), s));
+  B200_CUDA_TRY(scratch_alloc(&cor, (tiles + 1) * sizeof(uint64_t), s));
   int rc = merge_window_impl(a, la, b, lb, 0, la + lb, key_xor, out, cor, s);
   cudaFreeAsync(cor, s);
   return rc;
@@ -481,7 +606,7 @@ int b200_bitonic_merge_split_u32(const uint32_t* local, const uint32_t* partner,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const uint64_t tiles = (m + b200::kMergeTile - 1) / b200::kMergeTile;
   uint64_t* cor = nullptr;
-  B200_CUDA_TRY(cudaMallocAsync(&cor, (tiles + 1) * sizeof(uint64_t), s));
+  B200_CUDA_TRY(scratch_alloc(&cor, (tiles + 1) * sizeof(uint64_t), s));
   int rc = merge_split_impl(local, partner, m, keep_high, key_xor, out, cor, s);
   cudaFreeAsync(cor, s);
   return rc;

@@ -151,11 +151,13 @@ template <int C, int R>
 constexpr int threads_for() {
   return 1 << (C - R);
 }
-template <int C, int R>
+template <int C, int R, int MODE = 0>
 constexpr int min_blocks_for() {
-  // a 64-register budget per thread (1024 threads per SM at full use)
-  return threads_for<C, R>() >= 1024 ? 1
-         : (1024 / threads_for<C, R>() > 32 ? 32 : 1024 / threads_for<C, R>());
+  // a 64-register budget per thread (1024 threads per SM at full use); two
+  // register arrays of 32 keys get 128 registers (512 threads per SM)
+  constexpr int slots = (MODE != 0 && R >= 5) ? 512 : 1024;
+  return threads_for<C, R>() >= slots ? 1
+         : (slots / threads_for<C, R>() > 32 ? 32 : slots / threads_for<C, R>());
 }
 
 // ---- the pass body -------------------------------------------------------------
@@ -166,8 +168,13 @@ constexpr int min_blocks_for() {
 //   tile sort, phase C     : CTA-uniform          (DL = -1, value u[C])
 //   merge, phase A         : local bit C-1 when segment B follows, else uniform
 //   merge, phase B         : uniform
-template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), bool KV = false>
+// MODE 0: keys only.  MODE 1: key + 32-bit payload (the payload array
+// follows its key).  MODE 2: 64-bit keys split into a hi-word array (v) and
+// a lo-word array (w), compared lexicographically.
+template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), int MODE = 0>
 struct PassBody {
+  static constexpr bool KV = MODE != 0;   // two register arrays
+  static constexpr bool K64 = MODE == 2;
   using S = Seq<C, KIND, SA, SB>;
   static constexpr int R = RR;
   static constexpr int NR = 1 << R;
@@ -208,6 +215,7 @@ struct PassBody {
     uint32_t uA, uB;      // uniform direction masks (merge)
     uint32_t uC;          // uniform direction mask of phase C (tile sort)
     uint32_t gin, gout;   // key-order transforms
+    uint32_t gin_lo, gout_lo;  // low-word transforms (MODE 2)
   };
 
   // uniform mask for phase id ph when its direction bit is not local
@@ -255,8 +263,8 @@ struct PassBody {
   // When the runtime part is warp-uniform the branch is divergence-free and
   // only the registers that actually flip are complemented.
   template <class LR, int PH0, int PH1, bool EXTRA_WARP_UNIFORM>
-  __device__ __forceinline__ static void apply_mask(const Ctx& c, uint32_t (&v)[NR],
-                                                    uint32_t extra) {
+  __device__ __forceinline__ static void apply_mask1(const Ctx& c, uint32_t (&v)[NR],
+                                                     uint32_t extra) {
     constexpr int q0 = PH0 >= 0 ? reg_q<LR, PH0>() : -1;
     constexpr int q1 = PH1 >= 0 ? reg_q<LR, PH1>() : -1;
     // (measured: helps the ALU-bound tile sort, hurts the latency-bound
@@ -269,8 +277,8 @@ struct PassBody {
     if constexpr (PH1 >= 0) u ^= uni_part<LR, PH1>(c, tj);
     auto rbit = [](int e) -> bool {
       bool r = false;
-      if (q0 >= 0) r ^= ((e >> q0) & 1) != 0;
-      if (q1 >= 0) r ^= ((e >> q1) & 1) != 0;
+      if (q0 >= 0) r ^= ((e >> (q0 < 0 ? 0 : q0)) & 1) != 0;
+      if (q1 >= 0) r ^= ((e >> (q1 < 0 ? 0 : q1)) & 1) != 0;
       return r;
     };
     if constexpr (wu) {
@@ -294,10 +302,19 @@ struct PassBody {
     }
   }
 
+  // Keys (both words of a 64-bit key in MODE 2; payloads never change).
+  template <class LR, int PH0, int PH1, bool EXTRA_WARP_UNIFORM>
+  __device__ __forceinline__ static void apply_mask(const Ctx& c, uint32_t (&v)[NR],
+                                                    uint32_t (&w)[NR], uint32_t extra,
+                                                    uint32_t extra_lo) {
+    apply_mask1<LR, PH0, PH1, EXTRA_WARP_UNIFORM>(c, v, extra);
+    if constexpr (K64) apply_mask1<LR, PH0, PH1, EXTRA_WARP_UNIFORM>(c, w, extra_lo);
+  }
+
   template <class LR, int PH0, int PH1>
   __device__ __forceinline__ static void transition(const Ctx& c, uint32_t (&v)[NR],
-                                                    uint32_t extra) {
-    apply_mask<LR, PH0, PH1, true>(c, v, extra);
+                                                    uint32_t (&w)[NR]) {
+    apply_mask<LR, PH0, PH1, true>(c, v, w, 0u, 0u);
   }
 
   // Mask of register e, layout LR, phase id ph (0 / ~0).
@@ -324,10 +341,12 @@ struct PassBody {
     constexpr int ph = S::phase(I);
     constexpr int b = S::bit(I);
     if constexpr (natural(ph) && ph != 0) {
-      if constexpr (KV) LR::template ce_dir_kv<b, ph>(v, w);
+      if constexpr (K64) LR::template ce_dir_k64<b, ph>(v, w);
+      else if constexpr (KV) LR::template ce_dir_kv<b, ph>(v, w);
       else LR::template ce_dir<b, ph>(v);
     } else {
-      if constexpr (KV) LR::template ce_kv<b>(v, w);
+      if constexpr (K64) LR::template ce_k64<b>(v, w);
+      else if constexpr (KV) LR::template ce_kv<b>(v, w);
       else LR::template ce<b>(v);
     }
   }
@@ -337,7 +356,7 @@ struct PassBody {
                                                uint32_t (&w)[NR]) {
     if constexpr (I < RD::begin(r + 1)) {
       if constexpr (I > 0 && S::phase(I) != S::phase(I - 1)) {
-        transition<L<r>, S::phase(I - 1), S::phase(I)>(c, v, 0u);
+        transition<L<r>, S::phase(I - 1), S::phase(I)>(c, v, w);
       }
       one_step<L<r>, I>(v, w);
       steps<r, I + 1>(c, v, w);
@@ -414,12 +433,13 @@ struct PassBody {
         cv.keys = c.vals;
         gload<L0>(cv, tj, w);
       }
-      apply_mask<L0, PH, -1, true>(c, v, c.gin);
+      apply_mask<L0, PH, -1, true>(c, v, w, c.gin, c.gin_lo);
     } else {
       constexpr int db = natural(PH) ? -1 : dloc(PH);
       const uint32_t u = (natural(PH) || db >= 0) ? 0u : uni(c, PH);
       stage_in<C, A, db, R>(sm, c.keys, c.gbase, c.y, c.gin ^ u);
-      if constexpr (KV) stage_in<C, A, -1, R>(sm + TW, c.vals, c.gbase, c.y, 0u);
+      if constexpr (K64) stage_in<C, A, db, R>(sm + TW, c.vals, c.gbase, c.y, c.gin_lo ^ u);
+      else if constexpr (KV) stage_in<C, A, -1, R>(sm + TW, c.vals, c.gbase, c.y, 0u);
       L0::lds(sm, v);
       if constexpr (KV) L0::lds(sm + TW, w);
     }
@@ -431,7 +451,7 @@ struct PassBody {
     using LL = L<NRND - 1>;
     constexpr int PH = S::phase(S::len() - 1);
     const uint32_t tj = LL::thread_j();
-    apply_mask<LL, PH, -1, true>(c, v, c.gout);
+    apply_mask<LL, PH, -1, true>(c, v, w, c.gout, c.gout_lo);
     if constexpr (direct_ok<LL>()) {
       gstore<LL>(c, tj, v);
       if constexpr (KV) {
@@ -474,11 +494,11 @@ struct PassBody {
   }
 };
 
-template <int C, int R = reg_bits(C), bool KV = false>
-__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
+template <int C, int R = reg_bits(C), int MODE = 0>
+__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R, MODE>())
 tile_sort_kernel(PassParams P) {
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 0, -1, -1, R, KV>;
+  using B = PassBody<C, 0, -1, -1, R, MODE>;
   typename B::Ctx c;
   c.keys = P.keys;
   c.vals = P.vals;
@@ -488,15 +508,17 @@ tile_sort_kernel(PassParams P) {
   c.uC = 0u - dir_bit_global(c.gbase, C, P.kd);
   c.gin = P.gmask_in;
   c.gout = P.gmask_out;
+  c.gin_lo = P.gmask_in_lo;
+  c.gout_lo = P.gmask_out_lo;
   B::run(c, smem);
 }
 
-template <int C, int SA, int SB, int R = reg_bits(C), bool KV = false>
-__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
+template <int C, int SA, int SB, int R = reg_bits(C), int MODE = 0>
+__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R, MODE>())
 merge_kernel(PassParams P) {
   static_assert(SA >= 0 || SB >= 0, "empty pass");
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 1, SA, SB, R, KV>;
+  using B = PassBody<C, 1, SA, SB, R, MODE>;
   constexpr int A = B::A;
   typename B::Ctx c;
   c.keys = P.keys;
@@ -508,6 +530,8 @@ merge_kernel(PassParams P) {
   c.uC = 0u;
   c.gin = 0u;  // a merge pass never runs first: keys are already transformed
   c.gout = P.gmask_out;
+  c.gin_lo = 0u;
+  c.gout_lo = P.gmask_out_lo;
   B::run(c, smem);
 }
 

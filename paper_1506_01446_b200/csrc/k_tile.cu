@@ -4,26 +4,30 @@
 
 namespace b200 {
 
-PassFn find_tile_kernel(int C, int R, bool kv) {
-  if (kv) {
-    // key-value tiles: 16 pairs per thread (keys + payloads = 32 registers)
-    switch (C) {
-      case 1: return &tile_sort_kernel<1, 1, true>;
-      case 2: return &tile_sort_kernel<2, 2, true>;
-      case 3: return &tile_sort_kernel<3, 3, true>;
-      case 4: return &tile_sort_kernel<4, 4, true>;
-      case 5: return &tile_sort_kernel<5, 4, true>;
-      case 6: return &tile_sort_kernel<6, 4, true>;
-      case 7: return &tile_sort_kernel<7, 4, true>;
-      case 8: return &tile_sort_kernel<8, 4, true>;
-      case 9: return &tile_sort_kernel<9, 4, true>;
-      case 10: return &tile_sort_kernel<10, 4, true>;
-      case 11: return &tile_sort_kernel<11, 4, true>;
-      case 12: return &tile_sort_kernel<12, 4, true>;
-      case 13: return &tile_sort_kernel<13, 4, true>;
-      default: return nullptr;
-    }
+// key + payload tiles: 16 pairs per thread (keys + payloads = 32 registers)
+static PassFn kv_tile(int C) {
+  constexpr int MODE = 1;
+  switch (C) {
+    case 1: return &tile_sort_kernel<1, 1, MODE>;
+    case 2: return &tile_sort_kernel<2, 2, MODE>;
+    case 3: return &tile_sort_kernel<3, 3, MODE>;
+    case 4: return &tile_sort_kernel<4, 4, MODE>;
+    case 5: return &tile_sort_kernel<5, 4, MODE>;
+    case 6: return &tile_sort_kernel<6, 4, MODE>;
+    case 7: return &tile_sort_kernel<7, 4, MODE>;
+    case 8: return &tile_sort_kernel<8, 4, MODE>;
+    case 9: return &tile_sort_kernel<9, 4, MODE>;
+    case 10: return &tile_sort_kernel<10, 4, MODE>;
+    case 11: return &tile_sort_kernel<11, 4, MODE>;
+    case 12: return &tile_sort_kernel<12, 4, MODE>;
+    case 13: return &tile_sort_kernel<13, 4, MODE>;
+    default: return nullptr;
   }
+}
+
+PassFn find_tile_kernel(int C, int R, int mode) {
+  if (mode == 1) return R == (C < 4 ? C : 4) ? kv_tile(C) : nullptr;
+  if (mode == 2) return find_tile_kernel_k64(C, R);
   if (R == 4) {
     switch (C) {
       case 10: return &tile_sort_kernel<10, 4>;
@@ -60,12 +64,16 @@ struct Tables {
   MergeTable t[kMergeCMax + 1];
   MergeTable t4[kMergeCMax + 1];
   MergeTable tkv[kMergeCMax + 1];
+  MergeTable tk64[kMergeCMax + 1];
   Tables() {
     for (auto& x : t) x = MergeTable{};
     for (auto& x : t4) x = MergeTable{};
     for (auto& x : tkv) x = MergeTable{};
     fill_merge_table_12_kv(tkv[12]);
     fill_merge_table_13_kv(tkv[13]);
+    for (auto& x : tk64) x = MergeTable{};
+    fill_merge_table_12_k64(tk64[12]);
+    fill_merge_table_13_k64(tk64[13]);
     fill_merge_table_12_r4(t4[12]);
     fill_merge_table_13_r4(t4[13]);
     fill_merge_table_11(t[11]);
@@ -81,11 +89,13 @@ const Tables& tables() {
 }
 }  // namespace
 
-PassFn find_merge_kernel(int C, int SA, int SB, int R, bool kv) {
+PassFn find_merge_kernel(int C, int SA, int SB, int R, int mode) {
   if (C < kMergeCMin || C > kMergeCMax) return nullptr;
   if (R != 5 && R != 4) return nullptr;
-  if (kv && R != 4) return nullptr;
-  const MergeTable& t = kv ? tables().tkv[C] : (R == 5 ? tables().t[C] : tables().t4[C]);
+  if (mode != 0 && R != 4) return nullptr;
+  const MergeTable& t = mode == 1   ? tables().tkv[C]
+                        : mode == 2 ? tables().tk64[C]
+                                    : (R == 5 ? tables().t[C] : tables().t4[C]);
   if (SB >= 0 && SA == SB - 1 && SB < 16) return t.th[SB];
   if (SA < 0 && SB >= 0 && SB < 16) return t.ho[SB];
   if (SB < 0 && SA >= 0 && SA < 16) return t.to[SA];

@@ -9,11 +9,13 @@ using PassFn = void (*)(PassParams);
 
 // Tile-sort kernel for a 2^C tile (C in [1, 15]) with 2^R keys per thread
 // (R = 5, or R = 4 for the instantiated latency-bound sizes).
-PassFn find_tile_kernel(int C, int R = 5, bool kv = false);
+// mode: 0 keys only, 1 key + payload, 2 64-bit keys (hi/lo word arrays)
+PassFn find_tile_kernel(int C, int R = 5, int mode = 0);
 // Specialised merge kernel for local bits SA..0 then C-1..SB, or nullptr when
 // that shape was not instantiated (the caller then uses the runtime-dispatched
 // bitonic_pass_kernel<C>).
-PassFn find_merge_kernel(int C, int SA, int SB, int R = 5, bool kv = false);
+PassFn find_merge_kernel(int C, int SA, int SB, int R = 5, int mode = 0);
+PassFn find_tile_kernel_k64(int C, int R);  // k_tile_k64.cu
 
 // Instantiated merge tile sizes.
 constexpr int kMergeCMin = 11;
@@ -34,5 +36,7 @@ void fill_merge_table_12_r4(MergeTable& t);
 void fill_merge_table_13_r4(MergeTable& t);
 void fill_merge_table_12_kv(MergeTable& t);
 void fill_merge_table_13_kv(MergeTable& t);
+void fill_merge_table_12_k64(MergeTable& t);
+void fill_merge_table_13_k64(MergeTable& t);
 
 }  // namespace b200

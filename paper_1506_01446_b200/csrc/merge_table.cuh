@@ -8,26 +8,26 @@
 
 namespace b200 {
 
-template <int C, int A, int R, bool KV>
+template <int C, int A, int R, int MODE>
 PassFn th_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A, R, KV>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A, R, MODE>;
   else return nullptr;
 }
-template <int C, int A, int R, bool KV>
+template <int C, int A, int R, int MODE>
 PassFn ho_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A, R, KV>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A, R, MODE>;
   else return nullptr;
 }
-template <int C, int SA, int R, bool KV>
+template <int C, int SA, int R, int MODE>
 PassFn to_entry() {
-  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1, R, KV>;
+  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1, R, MODE>;
   else return nullptr;
 }
-template <int C, int R, bool KV, int... I>
+template <int C, int R, int MODE, int... I>
 void fill_merge_table(MergeTable& t, std::integer_sequence<int, I...>) {
-  ((t.th[I] = th_entry<C, I, R, KV>()), ...);
-  ((t.ho[I] = ho_entry<C, I, R, KV>()), ...);
-  ((t.to[I] = to_entry<C, I, R, KV>()), ...);
+  ((t.th[I] = th_entry<C, I, R, MODE>()), ...);
+  ((t.ho[I] = ho_entry<C, I, R, MODE>()), ...);
+  ((t.to[I] = to_entry<C, I, R, MODE>()), ...);
 }
 
 }  // namespace b200
@@ -35,20 +35,27 @@ void fill_merge_table(MergeTable& t, std::integer_sequence<int, I...>) {
 #define B200_DEFINE_MERGE_TABLE(CC)                                      \
   namespace b200 {                                                       \
   void fill_merge_table_##CC(MergeTable& t) {                            \
-    fill_merge_table<CC, 5, false>(t, std::make_integer_sequence<int, 16>{}); \
+    fill_merge_table<CC, 5, 0>(t, std::make_integer_sequence<int, 16>{}); \
   }                                                                      \
   }
 
 #define B200_DEFINE_MERGE_TABLE_R4(CC)                                   \
   namespace b200 {                                                       \
   void fill_merge_table_##CC##_r4(MergeTable& t) {                       \
-    fill_merge_table<CC, 4, false>(t, std::make_integer_sequence<int, 16>{}); \
+    fill_merge_table<CC, 4, 0>(t, std::make_integer_sequence<int, 16>{}); \
   }                                                                      \
   }
 
 #define B200_DEFINE_MERGE_TABLE_KV(CC)                                   \
   namespace b200 {                                                       \
   void fill_merge_table_##CC##_kv(MergeTable& t) {                       \
-    fill_merge_table<CC, 4, true>(t, std::make_integer_sequence<int, 16>{}); \
+    fill_merge_table<CC, 4, 1>(t, std::make_integer_sequence<int, 16>{}); \
+  }                                                                      \
+  }
+
+#define B200_DEFINE_MERGE_TABLE_K64(CC)                                  \
+  namespace b200 {                                                       \
+  void fill_merge_table_##CC##_k64(MergeTable& t) {                      \
+    fill_merge_table<CC, 4, 2>(t, std::make_integer_sequence<int, 16>{}); \
   }                                                                      \
   }

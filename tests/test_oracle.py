@@ -122,6 +122,29 @@ def test_zero_one_exhaustive(orc):
             assert (np.diff(out.astype(np.int64)) >= 0).all()
 
 
+def test_bitonic_64_orders(orc):
+    """64-bit oracle: uint64 / int64 orders equal a sort; float64 equals
+    IEEE totalOrder (bit patterns, so -0.0 < +0.0 and NaNs at the ends)."""
+    rng = np.random.default_rng(64)
+    for k in (1, 2, 5, 10):
+        for dt in (np.uint64, np.int64):
+            info = np.iinfo(dt)
+            x = rng.integers(info.min, info.max, size=1 << k, dtype=dt, endpoint=True)
+            x[: x.size // 2] = x[x.size // 2:]  # ties
+            for desc in (False, True):
+                want = np.sort(x)[::-1] if desc else np.sort(x)
+                assert (orc.bitonic_64(x, desc) == want).all()
+        f = rng.standard_normal(1 << k)
+        sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, -np.nan, 5e-324, -5e-324])
+        f[: min(f.size, sp.size)] = sp[: min(f.size, sp.size)]
+        u = f.view(np.uint64)
+        tok = np.where(u >> np.uint64(63) == 1, ~u, u | np.uint64(1 << 63))
+        want = f[np.argsort(tok, kind="stable")]
+        assert (orc.bitonic_64(f).view(np.uint64) == want.view(np.uint64)).all()
+    with pytest.raises(ValueError):
+        orc.bitonic_64(np.zeros(3, np.uint64))
+
+
 # ---- cross-check against the compiled reference itself -------------------
 
 def test_oracle_vs_reference_random(orc, ref):
