@@ -30,6 +30,7 @@ import subprocess
 import sys
 import threading
 import time
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -383,6 +384,11 @@ def main():
                      "definition": "P_min(k,15) x 8 B x n / measured HBM BW (SURVEY 8d)"}
 
     # ---- end to end through the public API with host buffers ---------------
+    # Single array: the reference-facing host entry (sort_host ->
+    # b200_bitonic_sort_host_u32, the drop-in for sequential_bitonic_sort),
+    # synchronous, timed on the host clock around the call; it copies H2D,
+    # sorts and copies D2H (chunk-pipelined) inside the call.  Batched: the
+    # device entry between explicit pinned copies, CUDA-event timed.
     e2e = None
     if world == 1:
         h_src = src.cpu().pin_memory()
@@ -391,22 +397,34 @@ def main():
         tt = []
         for i in range(args.warmup + args.steps):
             flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            dwork.copy_(h_src, non_blocking=True)
-            if batched:
-                b200.sort_batched_(dwork, batched)
+            if not batched:
+                h_out.copy_(h_src)  # restore the unsorted input (untimed)
+                torch.cuda.synchronize()
+                arr = h_out.view(torch.int32).numpy().view(np.uint32)
+                c0 = time.perf_counter()
+                b200.sort_host(arr)
+                t_ms = (time.perf_counter() - c0) * 1e3
             else:
-                b200.sort_(dwork)
-            h_out.copy_(dwork, non_blocking=True)
-            e1.record(stream)
-            torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                dwork.copy_(h_src, non_blocking=True)
+                b200.sort_batched_(dwork, batched)
+                h_out.copy_(dwork, non_blocking=True)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t_ms = e0.elapsed_time(e1)
             if i >= args.warmup:
-                tt.append(e0.elapsed_time(e1))
+                tt.append(t_ms)
+        if not batched:
+            ok = bool(np.all(arr[1:] >= arr[:-1]))
+            if not ok:
+                raise SystemExit("e2e host sort produced unsorted output")
         ems = sum(tt) / len(tt)
         e2e = {"value": n / (ems * 1e-3) / 1e9, "unit": "Gkeys/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
-               "ms_per_step": ems, "host_buffers": "pinned"}
+               "ms_per_step": ems, "host_buffers": "pinned",
+               "api": ("b200_bitonic_sort_host_u32 (host clock)" if not batched
+                       else "H2D + b200_bitonic_sort_u32_batched + D2H (CUDA events)")}
 
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
     cpu = None

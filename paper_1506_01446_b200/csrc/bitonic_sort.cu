@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -232,6 +233,135 @@ std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanO
   return plan;
 }
 
+// ---- CUDA graphs for repeated launches -------------------------------------
+// A sort is 1..31 dependent launches; enqueueing them costs ~3.5 us each on
+// the host, which at 2^20 keys is as long as the sort itself.  The second
+// time the same (device, buffers, shape, direction, tuning) is seen, the
+// launch sequence is captured once (on a private capture stream, so the
+// caller's stream may be the legacy default stream) and every later call
+// is a single cudaGraphLaunch on the caller's stream.  Calls made while the
+// caller's stream is itself being captured launch directly (they become
+// part of the caller's graph).  B200_BITONIC_GRAPHS=0 disables this.
+struct GraphKey {
+  int dev, kind, mode, desc, k, G;
+  const void* p0;
+  const void* p1;
+  uint64_t n, batch;
+  uint32_t kx;
+  int cmax, cmin, lrun, regbits, tile_regbits, dp, generic, pdl;
+  bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+struct GraphEntry {
+  GraphKey key;
+  int hits = 0;
+  cudaGraphExec_t exec = nullptr;
+};
+std::mutex g_graph_mu;
+std::vector<GraphEntry> g_graphs;
+thread_local cudaStream_t t_capture_stream[64] = {};
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("B200_BITONIC_GRAPHS");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+
+GraphKey make_key(int kind, const void* p0, const void* p1, uint64_t n, uint64_t batch,
+                  int desc, uint32_t kx, int mode, int G, const b200::PlanOptions& o) {
+  GraphKey key;
+  std::memset(&key, 0, sizeof(key));  // padding bytes take part in the compare
+  cudaGetDevice(&key.dev);
+  key.kind = kind;
+  key.p0 = p0;
+  key.p1 = p1;
+  key.n = n;
+  key.batch = batch;
+  key.desc = desc;
+  key.kx = kx;
+  key.mode = mode;
+  key.G = G;
+  key.cmax = o.cmax;
+  key.cmin = o.cmin;
+  key.lrun = o.lrun;
+  key.regbits = o.regbits;
+  key.tile_regbits = o.tile_regbits;
+  key.dp = o.dp;
+  key.generic = g_force_generic.load();
+  key.pdl = g_pdl.load();
+  return key;
+}
+
+// Runs fn(stream) directly, or through a cached graph once `key` repeats.
+template <class Fn>
+int run_graphed(const GraphKey& key, cudaStream_t s, Fn&& fn) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (!graphs_enabled() || cudaStreamIsCapturing(s, &st) != cudaSuccess ||
+      st != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return fn(s);
+  }
+  cudaGraphExec_t exec = nullptr;
+  bool capture = false;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = std::find_if(g_graphs.begin(), g_graphs.end(),
+                           [&](const GraphEntry& e) { return e.key == key; });
+    if (it == g_graphs.end()) {
+      if (g_graphs.size() >= 64) {
+        if (g_graphs.front().exec) cudaGraphExecDestroy(g_graphs.front().exec);
+        g_graphs.erase(g_graphs.begin());
+      }
+      GraphEntry e;
+      e.key = key;
+      e.hits = 1;
+      g_graphs.push_back(e);
+    } else {
+      exec = it->exec;
+      capture = exec == nullptr;
+      ++it->hits;
+    }
+  }
+  if (exec == nullptr && !capture) return fn(s);  // first sighting: launch directly
+  if (exec == nullptr) {
+    cudaStream_t& cs = t_capture_stream[key.dev & 63];
+    if (cs == nullptr) B200_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    B200_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int rc = fn(cs);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    if (rc != B200_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+    e = cudaGraphInstantiateWithFlags(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = std::find_if(g_graphs.begin(), g_graphs.end(),
+                           [&](const GraphEntry& x) { return x.key == key; });
+    if (it != g_graphs.end() && it->exec == nullptr) {
+      it->exec = exec;
+    } else {
+      // another thread won the race: launch ours once, keep theirs
+      cudaError_t le = cudaGraphLaunch(exec, s);
+      cudaGraphExecDestroy(exec);
+      return le == cudaSuccess ? B200_OK : cuda_fail(le, "graph launch");
+    }
+  }
+  B200_CUDA_TRY(cudaGraphLaunch(exec, s));
+  return B200_OK;
+}
+
+void drop_graphs() {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto& e : g_graphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  g_graphs.clear();
+}
+
 // Validates and runs the whole plan (or only pass `only`, when >= 0).
 // key_xor: 0x80000000 for int32 keys (for 64-bit keys: applied to the hi
 // word).  d_vals: payloads (mode 1) or the lo words of 64-bit keys whose hi
@@ -270,32 +400,39 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
   const uint32_t gmask_lo = (mode == 2 && descending) ? 0xFFFFFFFFu : 0u;
   if (only >= (int)plan.size()) return fail(B200_CONFIG, "pass index outside the plan");
-  for (size_t i = 0; i < plan.size(); ++i) {
-    if (only >= 0 && (int)i != only) continue;
-    const b200::PlanPass& q = plan[i];
-    b200::PassParams p{};
-    p.keys = d_keys;
-    p.vals = d_vals;
-    p.gmask_in = (i == 0) ? gmask : 0u;
-    p.gmask_out = (i + 1 == plan.size()) ? gmask : 0u;
-    p.gmask_in_lo = (i == 0) ? gmask_lo : 0u;
-    p.gmask_out_lo = (i + 1 == plan.size()) ? gmask_lo : 0u;
-    p.a = q.a;
-    p.y = q.y;
-    p.kd = k;
-    p.tile_sort = q.tile_sort;
-    p.p_end = q.p_end;
-    p.segA_hi = q.segA_hi;
-    p.pA = q.pA;
-    p.segB_lo = q.segB_lo;
-    p.pB = q.pB;
-    cudaError_t e = launch_pass(q, p, stream, mode);
-    if (e == cudaErrorNotSupported) {
-      return fail(B200_CONFIG, "no key-value kernel for this tile size (use tile_bits 0, 12 or 13)");
+  auto launch_all = [&](cudaStream_t st) -> int {
+    for (size_t i = 0; i < plan.size(); ++i) {
+      if (only >= 0 && (int)i != only) continue;
+      const b200::PlanPass& q = plan[i];
+      b200::PassParams p{};
+      p.keys = d_keys;
+      p.vals = d_vals;
+      p.gmask_in = (i == 0) ? gmask : 0u;
+      p.gmask_out = (i + 1 == plan.size()) ? gmask : 0u;
+      p.gmask_in_lo = (i == 0) ? gmask_lo : 0u;
+      p.gmask_out_lo = (i + 1 == plan.size()) ? gmask_lo : 0u;
+      p.a = q.a;
+      p.y = q.y;
+      p.kd = k;
+      p.tile_sort = q.tile_sort;
+      p.p_end = q.p_end;
+      p.segA_hi = q.segA_hi;
+      p.pA = q.pA;
+      p.segB_lo = q.segB_lo;
+      p.pB = q.pB;
+      cudaError_t e = launch_pass(q, p, st, mode);
+      if (e == cudaErrorNotSupported) {
+        return fail(B200_CONFIG,
+                    "no key-value kernel for this tile size (use tile_bits 0, 12 or 13)");
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "bitonic pass launch");
     }
-    if (e != cudaSuccess) return cuda_fail(e, "bitonic pass launch");
-  }
-  return B200_OK;
+    return B200_OK;
+  };
+  if (only >= 0 || plan.size() < 2) return launch_all(stream);
+  return run_graphed(make_key(0, d_keys, d_vals, n_per, batch, descending, key_xor, mode, 0,
+                              popt),
+                     stream, launch_all);
 }
 
 // ---- merge path ----------------------------------------------------------------
@@ -424,6 +561,199 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
   return rc;
 }
 
+
+// ---- host-span entry: pipelined H2D / sort / D2H ----------------------------
+// The reference's entry points sort host spans (sequential_bitonic_sort,
+// engine.hpp:102-104).  Here the span is cut into G chunks: chunk j's H2D
+// copy overlaps the bitonic sort of the chunks already on the device (one
+// stream per chunk); the sorted chunks are combined by a merge-path tree
+// (the merge kernels of the multi-GPU path), and the last merge is cut into
+// output windows so each window's D2H copy overlaps the merge of the next.
+// Device buffers and streams are cached per device (retained pool memory).
+struct HostPipe {
+  static constexpr int kMaxChunks = 8;
+  bool init = false;
+  cudaStream_t h2d = nullptr, d2h = nullptr, comp[kMaxChunks] = {};
+  std::vector<cudaEvent_t> ev;
+  std::mutex mu;
+  void* block = nullptr;  // device buffers, see pipe_buffers
+  size_t cap = 0;
+};
+std::mutex g_pipe_mu;
+std::vector<HostPipe*> g_pipes;
+
+HostPipe* host_pipe(int dev) {
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  if ((int)g_pipes.size() <= dev) g_pipes.resize(dev + 1, nullptr);
+  if (g_pipes[dev] == nullptr) g_pipes[dev] = new HostPipe();  // lives for the process
+  return g_pipes[dev];
+}
+
+cudaError_t pipe_init(HostPipe& P) {
+  if (P.init) return cudaSuccess;
+  cudaError_t e = cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking);
+  for (int j = 0; j < HostPipe::kMaxChunks && e == cudaSuccess; ++j)
+    e = cudaStreamCreateWithFlags(&P.comp[j], cudaStreamNonBlocking);
+  while (e == cudaSuccess && P.ev.size() < 64) {
+    cudaEvent_t x;
+    e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    if (e == cudaSuccess) P.ev.push_back(x);
+  }
+  if (e == cudaSuccess) P.init = true;
+  return e;
+}
+
+// Chunk count: chunks of >= 2^22 keys (16 MiB), at most 8 (measured on B200
+// + PCIe 5: up to 2^22 keys one chunk wins; at 2^24, 4 chunks save ~10%).
+int pipe_chunks(uint64_t n) {
+  if (const char* e = std::getenv("B200_BITONIC_HOST_CHUNKS")) {
+    int g = std::atoi(e);
+    if (g >= 1 && g <= HostPipe::kMaxChunks && (g & (g - 1)) == 0 && n / g >= 2) return g;
+  }
+  int g = 1;
+  while (g < HostPipe::kMaxChunks && n / (uint64_t)(2 * g) >= (uint64_t{1} << 22)) g *= 2;
+  return g;
+}
+
+// Device buffers for the host entry: [A: n keys | B: n keys | coranks],
+// one allocation per device, grown on demand and kept (graphs refer to it).
+cudaError_t pipe_buffers(HostPipe& P, uint64_t n, uint64_t cor_words) {
+  const size_t need = n * 8 + cor_words * 8;
+  if (P.cap >= need) return cudaSuccess;
+  if (P.block) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
+    drop_graphs();  // captured pipelines refer to the old block
+    cudaFree(P.block);
+    P.block = nullptr;
+    P.cap = 0;
+  }
+  cudaError_t e = cudaMalloc(&P.block, need);
+  if (e == cudaSuccess) P.cap = need;
+  return e;
+}
+
+int host_sort(uint32_t* h, uint64_t n, int descending, uint32_t key_xor) {
+  if (n < 2 || !is_pow2(n)) {
+    return fail(B200_INVALID_SIZE,
+                "length must be a power of two >= 2, got " + std::to_string(n));
+  }
+  if (h == nullptr) return fail(B200_CONFIG, "null key pointer");
+  if (descending != 0 && descending != 1) {
+    return fail(B200_CONFIG, "descending must be 0 or 1");
+  }
+  int dev = 0;
+  B200_CUDA_TRY(cudaGetDevice(&dev));
+  HostPipe& P = *host_pipe(dev);
+  std::lock_guard<std::mutex> lk(P.mu);
+  B200_CUDA_TRY(pipe_init(P));
+  const int G = pipe_chunks(n);
+  const uint64_t c = n / G;
+  const uint32_t kx = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+  const uint64_t cor_per_round = n / b200::kMergeTile + 2 * HostPipe::kMaxChunks + 2;
+  int rounds = 0;
+  while ((1 << rounds) < G) ++rounds;
+  B200_CUDA_TRY(pipe_buffers(P, n, cor_per_round * (rounds + 1)));
+  uint32_t* A = reinterpret_cast<uint32_t*>(P.block);
+  uint32_t* B = A + n;
+  uint64_t* cor = reinterpret_cast<uint64_t*>(B + n);
+
+  // The whole pipeline, forked from and joined back into `origin`.
+  auto pipeline = [&](cudaStream_t origin) -> int {
+    int rc = B200_OK;
+    size_t evi = 0;
+    auto dep = [&](cudaStream_t from, cudaStream_t to) {
+      if (from == to) return;
+      cudaEvent_t x = P.ev[evi++ % P.ev.size()];
+      cudaEventRecord(x, from);
+      cudaStreamWaitEvent(to, x, 0);
+    };
+    if (G == 1) {
+      cudaError_t e = cudaMemcpyAsync(A, h, n * 4, cudaMemcpyHostToDevice, origin);
+      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+      rc = sort_impl(A, n, 1, descending, key_xor, origin);
+      if (rc != B200_OK) return rc;
+      e = cudaMemcpyAsync(h, A, n * 4, cudaMemcpyDeviceToHost, origin);
+      return e == cudaSuccess ? B200_OK : cuda_fail(e, "D2H copy");
+    }
+    dep(origin, P.h2d);
+    for (int j = 0; j < G; ++j) dep(origin, P.comp[j]);
+    // 1. chunk j: H2D on the copy stream, then its sort on stream j
+    for (int j = 0; j < G && rc == B200_OK; ++j) {
+      cudaError_t e = cudaMemcpyAsync(A + j * c, h + j * c, c * 4, cudaMemcpyHostToDevice,
+                                      P.h2d);
+      if (e != cudaSuccess) {
+        rc = cuda_fail(e, "H2D copy");
+        break;
+      }
+      dep(P.h2d, P.comp[j]);
+      rc = sort_impl(A + j * c, c, 1, descending, key_xor, P.comp[j]);
+    }
+    // 2. merge tree: run r lives on stream comp[owner[r]]
+    std::vector<int> owner(G);
+    for (int j = 0; j < G; ++j) owner[j] = j;
+    uint32_t* src = A;
+    uint32_t* dst = B;
+    uint64_t len = c;
+    int runs = G, round = 0;
+    while (runs > 2 && rc == B200_OK) {
+      std::vector<int> nowner(runs / 2);
+      for (int q = 0; q < runs / 2 && rc == B200_OK; ++q) {
+        cudaStream_t sq = P.comp[owner[2 * q]];
+        dep(P.comp[owner[2 * q + 1]], sq);
+        uint64_t* cq = cor + round * cor_per_round + q * (2 * len / b200::kMergeTile + 2);
+        rc = merge_window_impl(src + 2 * q * len, len, src + (2 * q + 1) * len, len, 0,
+                               2 * len, kx, dst + 2 * q * len, cq, sq);
+        nowner[q] = owner[2 * q];
+      }
+      owner = nowner;
+      std::swap(src, dst);
+      len *= 2;
+      runs /= 2;
+      ++round;
+    }
+    // 3. last merge in output windows, each copied back as soon as it is done
+    if (rc == B200_OK) {
+      cudaStream_t sm = P.comp[owner[0]];
+      dep(P.comp[owner[1]], sm);
+      const int W = G;
+      const uint64_t ow = n / W;
+      uint64_t* cw = cor + round * cor_per_round;
+      for (int w = 0; w < W && rc == B200_OK; ++w) {
+        rc = merge_window_impl(src, len, src + len, len, w * ow, ow, kx, dst + w * ow, cw, sm);
+        if (rc != B200_OK) break;
+        dep(sm, P.d2h);
+        cudaError_t e = cudaMemcpyAsync(h + w * ow, dst + w * ow, ow * 4,
+                                        cudaMemcpyDeviceToHost, P.d2h);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
+      }
+    }
+    // join every stream back into the origin
+    dep(P.d2h, origin);
+    dep(P.h2d, origin);
+    for (int j = 0; j < G; ++j) dep(P.comp[j], origin);
+    return rc;
+  };
+
+  // Graph only page-locked spans (a pageable copy cannot be captured).
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, h) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  cudaStream_t s0 = P.comp[0];
+  int rc;
+  if (pinned) {
+    rc = run_graphed(make_key(1, h, P.block, n, 1, descending, key_xor, 0, G, plan_options()),
+                     s0, pipeline);
+  } else {
+    rc = pipeline(s0);
+  }
+  cudaError_t e = cudaStreamSynchronize(s0);
+  if (rc == B200_OK && e != cudaSuccess) rc = cuda_fail(e, "host sort");
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -493,6 +823,18 @@ int b200_bitonic_sort_u64_planes(uint32_t* d_hi, uint32_t* d_lo, uint64_t n,
 }
 
 int b200_bitonic_release_scratch(void) {
+  drop_graphs();
+  {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    for (HostPipe* hp : g_pipes) {
+      if (hp == nullptr || hp->block == nullptr) continue;
+      std::lock_guard<std::mutex> lk2(hp->mu);
+      if (hp->init) cudaStreamSynchronize(hp->comp[0]);
+      cudaFree(hp->block);
+      hp->block = nullptr;
+      hp->cap = 0;
+    }
+  }
   std::lock_guard<std::mutex> lk(g_pool_mu);
   for (cudaMemPool_t p : g_pools) {
     if (p == nullptr) continue;
@@ -538,35 +880,6 @@ int b200_bitonic_sort_i32_batched(int32_t* d_keys, uint64_t n_per_array,
   return sort_impl(reinterpret_cast<uint32_t*>(d_keys), n_per_array, batch,
                    descending, 0x80000000u,
                    reinterpret_cast<cudaStream_t>(stream));
-}
-
-static int host_sort(uint32_t* h, uint64_t n, int descending, uint32_t key_xor) {
-  if (n < 2 || !is_pow2(n)) {
-    return fail(B200_INVALID_SIZE,
-                "length must be a power of two >= 2, got " + std::to_string(n));
-  }
-  if (h == nullptr) return fail(B200_CONFIG, "null key pointer");
-  uint32_t* d = nullptr;
-  cudaStream_t s = nullptr;
-  B200_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  cudaError_t e = scratch_alloc(&d, n * 4, s);
-  if (e != cudaSuccess) {
-    cudaStreamDestroy(s);
-    return cuda_fail(e, "scratch allocation");
-  }
-  int rc = B200_OK;
-  e = cudaMemcpyAsync(d, h, n * 4, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) rc = cuda_fail(e, "H2D copy");
-  if (rc == B200_OK) rc = sort_impl(d, n, 1, descending, key_xor, s);
-  if (rc == B200_OK) {
-    e = cudaMemcpyAsync(h, d, n * 4, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
-  }
-  cudaFreeAsync(d, s);
-  e = cudaStreamSynchronize(s);
-  if (rc == B200_OK && e != cudaSuccess) rc = cuda_fail(e, "sort");
-  cudaStreamDestroy(s);
-  return rc;
 }
 
 int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending) {
