@@ -202,12 +202,12 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   t.ctas = total >> C;
   t.ces = (total / 2) * (uint64_t)(t.p_end * (t.p_end + 1) / 2);
   plan.push_back(t);
-  // 16 keys per thread (twice the warps per SM) up to 2^19 keys, where the
+  // 16 keys per thread (twice the warps per SM) up to 2^21 keys, where the
   // passes are latency-bound, and for batched tiles (ALU-bound: more warps
   // overlap the shared-memory rounds); 32 keys per thread elsewhere
   // (measured on B200).
   int R = opt.regbits > 0 ? opt.regbits
-                          : ((k <= 19 && batch == 1) || (batch > 1 && C >= 10 && C <= 14) ? 4 : 5);
+                          : ((k <= 21 && batch == 1) || (batch > 1 && C >= 10 && C <= 14) ? 4 : 5);
   if (opt.kv) R = C < 4 ? C : 4;
   for (auto& q : plan) q.R = R;
   if (opt.tile_regbits > 0 && !opt.kv) plan.front().R = opt.tile_regbits;
