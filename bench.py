@@ -135,6 +135,8 @@ def reference_arm(args):
     ref = oracle.reference()
     n = 1 << args.log2n
     cores = os.cpu_count() or 1
+    if args.batched:
+        return reference_arm_batched(args, ref, n, cores)
     if ref is not None:
         kind = "reference"
         rng = np.random.default_rng(1)
@@ -176,6 +178,111 @@ def reference_arm(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _array_sample(n_per: int, total_arrays: int, target_keys: int = 1 << 22):
+    """A bounded sample of the batched workload: the first arrays of the same
+    generator stream, about target_keys keys in all."""
+    import numpy as np
+    count = max(1, min(total_arrays, target_keys // n_per))
+    rng = np.random.default_rng(1)
+    x = rng.integers(-2**31, 2**31, count * n_per, dtype=np.int64).astype(np.int32)
+    return x.reshape(count, n_per)
+
+
+def _per_array_parallel(fn, arrays, cores):
+    """fn on every row, rows spread over `cores` threads (the ctypes calls
+    release the GIL, so the reference code runs on all cores)."""
+    from concurrent.futures import ThreadPoolExecutor
+    rows = list(arrays)
+    if cores <= 1:
+        for r in rows:
+            fn(r)
+        return
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(fn, rows))
+
+
+def reference_arm_batched(args, ref, n, cores):
+    """Reference arm for the batched config: the reference's own
+    sequential_bitonic_sort on every array of a bounded sample of the
+    workload, arrays spread over all host cores (the reference has no batched
+    entry; one array per call is its API)."""
+    import numpy as np
+    n_per = args.batched
+    x = _array_sample(n_per, n // n_per)
+    work = x.copy()
+    if ref is not None:
+        kind, fn = "reference", ref.sequential_bitonic_sort_inplace
+        what = (f"bitonic::sequential_bitonic_sort on {x.shape[0]} of the {n // n_per} "
+                f"arrays of {n_per} keys, {cores} threads")
+    else:  # pragma: no cover
+        import oracle
+        o = oracle.oracle()
+        kind = "port"
+        fn = lambda a: a.__setitem__(slice(None), o.sequential_bitonic_i32(a))
+        what = f"oracle sequential_bitonic_i32 on {x.shape[0]} arrays, {cores} threads"
+    for _ in range(args.warmup):
+        work[:] = x
+        _per_array_parallel(fn, work, cores)
+    times = []
+    for _ in range(args.steps):
+        work[:] = x
+        t0 = time.perf_counter()
+        _per_array_parallel(fn, work, cores)
+        times.append(time.perf_counter() - t0)
+    assert (np.diff(work.astype(np.int64), axis=1) >= 0).all()
+    ms = 1e3 * sum(times) / len(times)
+    value = work.size / (ms * 1e-3) / 1e9
+    world, _, _ = dist_env()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gkeys/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms * (n / work.size), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"batched: {n // n_per} arrays of {n_per} random uint32 "
+                               f"keys (CPU, sampled)", "keys": n,
+                   "sample_keys": int(work.size)},
+        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": cores,
+                         "kind": kind, "sample": what},
+        "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_batched(n_per: int, total_arrays: int, budget_s: float = 12.0):
+    """Batched workload on the host: the paper's quicksort per array (1 core)
+    and the reference's sequential bitonic per array over all cores, on a
+    bounded sample of the arrays."""
+    import oracle
+    ref = oracle.reference()
+    x = _array_sample(n_per, total_arrays)
+    cores = os.cpu_count() or 1
+    if ref is None:
+        o = oracle.oracle()
+        kind = "port"
+        qs = lambda a: a.__setitem__(slice(None), o.quicksort_i32(a))
+        seq = lambda a: a.__setitem__(slice(None), o.sequential_bitonic_i32(a))
+    else:
+        kind, qs, seq = "reference", ref.quicksort_inplace, ref.sequential_bitonic_sort_inplace
+    t_start = time.perf_counter()
+
+    def best(fn, c, reps):
+        b = float("inf")
+        for _ in range(reps):
+            w = x.copy()
+            t0 = time.perf_counter()
+            _per_array_parallel(fn, w, c)
+            b = min(b, time.perf_counter() - t0)
+            if time.perf_counter() - t_start > budget_s:
+                break
+        return b
+    out = {"sample_arrays": int(x.shape[0]), "sample_keys": int(x.size)}
+    out["quicksort_ms"] = 1e3 * best(qs, 1, 3)
+    out["sequential_bitonic_all_cores_ms"] = 1e3 * best(seq, cores, 3)
+    return kind, cores, out
 
 
 def cpu_baseline(n: int, budget_s: float = 12.0):
@@ -366,8 +473,8 @@ def main():
         try:  # measured DRAM bytes per launch from the committed ncu capture
             with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
                 tr = json.load(f)
-            if not batched:
-                traffic = tr.get(str(args.log2n), {}).get(dom)
+            key = f"batched{batched}" if batched else str(args.log2n)
+            traffic = tr.get(key, {}).get(dom)
         except Exception:
             pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
@@ -428,6 +535,23 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
     cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline and batched:
+        try:
+            kind, cores, c = cpu_baseline_batched(batched, n // batched)
+            qs_gk = c["sample_keys"] / (c["quicksort_ms"] * 1e-3) / 1e9
+            cpu = {"value": qs_gk, "unit": "Gkeys/s", "cores": 1, "kind": kind,
+                   "sample": f"bitonic::reference_quicksort on each of the first "
+                             f"{c['sample_arrays']} of the {n // batched} arrays of "
+                             f"{batched} keys (1 core), min of reps",
+                   "quicksort_ms": c["quicksort_ms"],
+                   "sequential_bitonic_all_cores_ms": c["sequential_bitonic_all_cores_ms"],
+                   "sequential_bitonic_all_cores_gkeys": c["sample_keys"] / (
+                       c["sequential_bitonic_all_cores_ms"] * 1e-3) / 1e9,
+                   "all_cores": cores,
+                   "speedup_vs_quicksort": value / qs_gk}
+        except Exception as e:  # pragma: no cover - report, do not fail the bench
+            cpu = {"value": None, "unit": "Gkeys/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"cpu baseline failed: {e}"}
     if world == 1 and rank == 0 and not args.no_cpu_baseline and not batched:
         try:
             kind, cores, c = cpu_baseline(n)
