@@ -133,10 +133,13 @@ def reference_arm(args):
     import numpy as np
     import oracle
     ref = oracle.reference()
-    n = 1 << args.log2n
+    n_config = (1 << args.log2n) * world
     cores = os.cpu_count() or 1
     if args.batched:
-        return reference_arm_batched(args, ref, n, cores)
+        return reference_arm_batched(args, ref, 1 << args.log2n, cores)
+    # bounded sample of the configuration (the reference's CPU sort of 2^32
+    # keys would take minutes per step); throughput is per key
+    n = min(n_config, 1 << 22)
     if ref is not None:
         kind = "reference"
         rng = np.random.default_rng(1)
@@ -144,6 +147,8 @@ def reference_arm(args):
         work = x.copy()
         run = lambda: ref.execute_inplace(work, 2, min(1024, n), cores)
         what = f"bitonic::execute(build_plan(fused, {min(1024, n)}), keys, {cores} workers)"
+        if n < n_config:
+            what += f" on a 2^{n.bit_length() - 1}-key sample of the 2^{n_config.bit_length() - 1}-key workload"
     else:  # pragma: no cover - oracle port when the reference was not built
         kind = "port"
         o = oracle.oracle()
@@ -167,10 +172,11 @@ def reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gkeys/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"2^{args.log2n} random uint32 keys, ascending (CPU)",
-                   "keys": n},
+        "config": {"workload": (f"2^{n_config.bit_length() - 1} random uint32 keys, ascending "
+                                f"(CPU{', sampled' if n < n_config else ''})"),
+                   "keys": n_config, "sample_keys": n},
         "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": cores,
                          "kind": kind, "sample": what},
         "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
@@ -334,13 +340,25 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--log2n", type=int, default=20,
-                    help="keys per GPU = 2^log2n (default 20 = BASELINE configs[1])")
+    ap.add_argument("--log2n", type=int, default=None,
+                    help="keys per GPU = 2^log2n.  Default: 20 at N=1 (BASELINE "
+                         "configs[1]); 32 - log2(N) at N>1 (configs[4]: 2^32 keys "
+                         "partitioned over the N GPUs); 24 with --batched (configs[3])")
     ap.add_argument("--batched", type=int, default=0,
                     help="n_per_array for the batched config (e.g. 4096)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    args.scaling = "weak"
+    if args.log2n is None:
+        world0 = dist_env()[0]
+        if args.batched:
+            args.log2n = 24
+        elif world0 > 1:
+            args.log2n = 32 - (world0.bit_length() - 1)
+            args.scaling = "strong"  # 2^32 keys in all, whatever N
+        else:
+            args.log2n = 20
 
     if args.impl == "reference":
         return reference_arm(args)
@@ -533,6 +551,46 @@ def main():
                "api": ("b200_bitonic_sort_host_u32 (host clock)" if not batched
                        else "H2D + b200_bitonic_sort_u32_batched + D2H (CUDA events)")}
 
+    if world > 1:
+        # Each rank: H2D of its shard from pinned host memory, the partitioned
+        # sort, D2H of its sorted shard; host clock, max over ranks.  Few
+        # steps (restoring GiB-sized pinned buffers on the host is slow).
+        err = None
+        try:
+            h_src = src.cpu().pin_memory()
+            h_work = torch.empty_like(h_src).pin_memory()
+        except Exception as ex:  # pragma: no cover
+            err = repr(ex)[:200]
+        okf = torch.tensor([0 if err else 1], device=dev, dtype=torch.int32)
+        dist.all_reduce(okf, op=dist.ReduceOp.MIN)  # every rank agrees before timing
+        if int(okf.item()) == 1:
+            tt = []
+            e_steps = min(args.steps, 3)
+            for i in range(1 + e_steps):
+                h_work.copy_(h_src)
+                torch.cuda.synchronize()
+                barrier()
+                c0 = time.perf_counter()
+                work.copy_(h_work, non_blocking=True)
+                sort_step()
+                h_work.copy_(work, non_blocking=True)
+                torch.cuda.synchronize()
+                t_ms = (time.perf_counter() - c0) * 1e3
+                t = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                if i >= 1:
+                    tt.append(float(t.item()))
+            ems = sum(tt) / len(tt)
+            e2e = {"value": keys_total / (ems * 1e-3) / 1e9, "unit": "Gkeys/s",
+                   "h2d_bytes_per_step": 4 * keys_total, "d2h_bytes_per_step": 4 * keys_total,
+                   "ms_per_step": ems, "steps": e_steps, "host_buffers": "pinned, one per rank",
+                   "api": "H2D + paper_1506_01446_b200.dist.partitioned_sort_ + D2H per rank "
+                          "(host clock, max over ranks)"}
+        else:  # pragma: no cover - report instead of failing the bench
+            e2e = {"value": None, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * keys_total,
+                   "d2h_bytes_per_step": 4 * keys_total,
+                   "error": err or "pinned host buffers unavailable on some rank"}
+
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline and batched:
@@ -572,7 +630,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u32", "data": "synthetic",
             "config": {"workload": workload, "keys_per_gpu": n, "keys_total": keys_total,
                        "l2_flush": "256 MiB write before every step (outside timing)",
