@@ -14,8 +14,10 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libb200_bitonic.so")
+# Experiment hooks: B200_BITONIC_OBJ / B200_BITONIC_LIBOUT redirect the object
+# directory and the library; B200_BITONIC_EXTRA_NVCC adds flags (e.g. -D...).
+OBJ = os.environ.get("B200_BITONIC_OBJ") or os.path.join(ROOT, "build", "obj")
+LIB = os.environ.get("B200_BITONIC_LIBOUT") or os.path.join(HERE, "libb200_bitonic.so")
 SOURCES = [os.path.join(CSRC, f) for f in
            ["bitonic_sort.cu", "k_tile.cu", "k_merge11.cu", "k_merge12.cu",
             "k_merge13.cu", "k_merge14.cu", "k_merge15.cu", "k_merge12r4.cu",
@@ -27,7 +29,7 @@ HEADERS.append(os.path.join(ROOT, "include", "b200_bitonic.h"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
-                     "-Xptxas", "-warn-spills"]
+                     "-Xptxas", "-warn-spills"] + os.environ.get("B200_BITONIC_EXTRA_NVCC", "").split()
 
 
 def nvcc() -> str:

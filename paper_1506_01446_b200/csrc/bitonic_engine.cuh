@@ -82,6 +82,14 @@ struct PassParams {
   // Segment B (head / middle of a phase): CEs on local bits C-1..segB_lo.
   int segB_lo;        // -1 when absent
   int pB;
+  // 1 and 0xFFFFFFFF, opaque to the compiler: operands of the IMAD form of
+  // max() that moves part of the compare-exchange work to the FMA pipe
+  uint32_t one, mone;
+};
+
+// Operands of the FMA-pipe max (see Layout::mm).
+struct FmaSplit {
+  uint32_t one, mone;
 };
 
 template <int C>

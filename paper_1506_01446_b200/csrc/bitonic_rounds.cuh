@@ -29,6 +29,22 @@
 
 #include "bitonic_engine.cuh"
 
+// CEs whose max runs on the FMA pipe: NUM of every DEN (measured on B200:
+// 2/3 for the merge passes, 1/3 for the tile sort, whose issue slots and
+// shared-memory pipe are as busy as its ALU pipe).
+#ifndef B200_FMA_NUM
+#define B200_FMA_NUM 2
+#endif
+#ifndef B200_FMA_DEN
+#define B200_FMA_DEN 3
+#endif
+#ifndef B200_FMA_TILE_NUM
+#define B200_FMA_TILE_NUM 1
+#endif
+#ifndef B200_FMA_TILE_DEN
+#define B200_FMA_TILE_DEN 3
+#endif
+
 namespace b200 {
 
 // ---- compile-time step sequences -----------------------------------------
@@ -293,33 +309,52 @@ struct Layout {
 #pragma unroll
     for (int e = 0; e < NR; ++e) v[e] = sm[b + reg_off(e)];
   }
+  // min and max of one compare-exchange.  VIMNMX issues at 64/clk/SM on the
+  // ALU pipe, so a CE costs two ALU slots; for two CEs in three, max is
+  // computed as x + y - min by two IMADs on the otherwise idle FMA pipe
+  // (exact in mod-2^32 arithmetic).  tools/mb_minmax.cu: 45 CE/clk/SM with
+  // this 2:1 split vs 32 with VIMNMX pairs.  `one`/`mone` come from the
+  // kernel parameters so ptxas cannot turn the IMADs back into IADD3s.
+  template <int NUM, int DEN>
+  __device__ __forceinline__ static void mm(int idx, uint32_t x, uint32_t y, uint32_t& lo,
+                                            uint32_t& hi, FmaSplit f) {
+    lo = min(x, y);
+    if (idx % DEN < NUM) {
+      uint32_t s;
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(x), "r"(f.one), "r"(y));
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"(lo), "r"(f.mone), "r"(s));
+    } else {
+      hi = max(x, y);
+    }
+  }
   // CE on local bit B (ascending in the phase domain)
-  template <int B>
-  __device__ __forceinline__ static void ce(uint32_t (&v)[NR]) {
+  template <int B, int NUM, int DEN>
+  __device__ __forceinline__ static void ce(uint32_t (&v)[NR], FmaSplit f) {
     constexpr int q = qof(B);
     static_assert(q >= 0, "CE bit must be a register bit");
 #pragma unroll
     for (int e = 0; e < NR; ++e) {
       if (!(e & (1 << q))) {
-        const uint32_t x = v[e], y = v[e | (1 << q)];
-        v[e] = min(x, y);
-        v[e | (1 << q)] = max(x, y);
+        const int idx = (e & ((1 << q) - 1)) | ((e >> (q + 1)) << q);
+        mm<NUM, DEN>(idx, v[e], v[e | (1 << q)], v[e], v[e | (1 << q)], f);
       }
     }
   }
   // CE on local bit B, direction from local bit D (a register bit)
-  template <int B, int D>
-  __device__ __forceinline__ static void ce_dir(uint32_t (&v)[NR]) {
+  template <int B, int D, int NUM, int DEN>
+  __device__ __forceinline__ static void ce_dir(uint32_t (&v)[NR], FmaSplit f) {
     constexpr int q = qof(B);
     constexpr int qd = qof(D);
     static_assert(q >= 0 && qd >= 0, "CE and direction bits must be register bits");
 #pragma unroll
     for (int e = 0; e < NR; ++e) {
       if (!(e & (1 << q))) {
-        const uint32_t x = v[e], y = v[e | (1 << q)];
+        const int idx = (e & ((1 << q) - 1)) | ((e >> (q + 1)) << q);
+        uint32_t lo, hi;
+        mm<NUM, DEN>(idx, v[e], v[e | (1 << q)], lo, hi, f);
         const bool desc = (e >> qd) & 1;
-        v[e] = desc ? max(x, y) : min(x, y);
-        v[e | (1 << q)] = desc ? min(x, y) : max(x, y);
+        v[e] = desc ? hi : lo;
+        v[e | (1 << q)] = desc ? lo : hi;
       }
     }
   }

@@ -420,6 +420,8 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
       p.pA = q.pA;
       p.segB_lo = q.segB_lo;
       p.pB = q.pB;
+      p.one = 1u;
+      p.mone = 0xFFFFFFFFu;
       cudaError_t e = launch_pass(q, p, st, mode);
       if (e == cudaErrorNotSupported) {
         return fail(B200_CONFIG,

@@ -174,6 +174,9 @@ constexpr int min_blocks_for() {
 template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), int MODE = 0>
 struct PassBody {
   static constexpr bool KV = MODE != 0;   // two register arrays
+  // FMA-pipe share of the compare-exchange max (Layout::mm)
+  static constexpr int FN = KIND == 0 ? B200_FMA_TILE_NUM : B200_FMA_NUM;
+  static constexpr int FD = KIND == 0 ? B200_FMA_TILE_DEN : B200_FMA_DEN;
   static constexpr bool K64 = MODE == 2;
   using S = Seq<C, KIND, SA, SB>;
   static constexpr int R = RR;
@@ -216,6 +219,7 @@ struct PassBody {
     uint32_t uC;          // uniform direction mask of phase C (tile sort)
     uint32_t gin, gout;   // key-order transforms
     uint32_t gin_lo, gout_lo;  // low-word transforms (MODE 2)
+    FmaSplit fs;               // opaque 1 / -1 (FMA-pipe max)
   };
 
   // uniform mask for phase id ph when its direction bit is not local
@@ -337,17 +341,18 @@ struct PassBody {
   }
 
   template <class LR, int I>
-  __device__ __forceinline__ static void one_step(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+  __device__ __forceinline__ static void one_step(const Ctx& c, uint32_t (&v)[NR],
+                                                  uint32_t (&w)[NR]) {
     constexpr int ph = S::phase(I);
     constexpr int b = S::bit(I);
     if constexpr (natural(ph) && ph != 0) {
       if constexpr (K64) LR::template ce_dir_k64<b, ph>(v, w);
       else if constexpr (KV) LR::template ce_dir_kv<b, ph>(v, w);
-      else LR::template ce_dir<b, ph>(v);
+      else LR::template ce_dir<b, ph, FN, FD>(v, c.fs);
     } else {
       if constexpr (K64) LR::template ce_k64<b>(v, w);
       else if constexpr (KV) LR::template ce_kv<b>(v, w);
-      else LR::template ce<b>(v);
+      else LR::template ce<b, FN, FD>(v, c.fs);
     }
   }
 
@@ -358,7 +363,7 @@ struct PassBody {
       if constexpr (I > 0 && S::phase(I) != S::phase(I - 1)) {
         transition<L<r>, S::phase(I - 1), S::phase(I)>(c, v, w);
       }
-      one_step<L<r>, I>(v, w);
+      one_step<L<r>, I>(c, v, w);
       steps<r, I + 1>(c, v, w);
     }
   }
@@ -510,6 +515,7 @@ tile_sort_kernel(PassParams P) {
   c.gout = P.gmask_out;
   c.gin_lo = P.gmask_in_lo;
   c.gout_lo = P.gmask_out_lo;
+  c.fs = FmaSplit{P.one, P.mone};
   B::run(c, smem);
 }
 
@@ -532,6 +538,7 @@ merge_kernel(PassParams P) {
   c.gout = P.gmask_out;
   c.gin_lo = 0u;
   c.gout_lo = P.gmask_out_lo;
+  c.fs = FmaSplit{P.one, P.mone};
   B::run(c, smem);
 }
 
