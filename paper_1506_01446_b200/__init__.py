@@ -105,6 +105,20 @@ def _key_dtype32(t):
     return kind
 
 
+def _on_device(t):
+    """Make t's device current for the native call (the library launches on
+    the current device and uses that device's current stream)."""
+    import torch
+    return torch.cuda.device(t.device)
+
+
+def _same_device(*ts) -> None:
+    d = ts[0].device
+    for t in ts[1:]:
+        if t.device != d:
+            raise ConfigError(f"tensors on different devices: {d} and {t.device}")
+
+
 def _check_tensor(t) -> None:
     if not t.is_cuda:
         raise ConfigError("sort_ needs a CUDA tensor (use sort_host for host arrays)")
@@ -122,8 +136,9 @@ def sort_(t, descending: bool = False, stream=None):
     fn = {"i32": L.b200_bitonic_sort_i32, "u32": L.b200_bitonic_sort_u32,
           "f32": L.b200_bitonic_sort_f32, "i64": L.b200_bitonic_sort_i64,
           "u64": L.b200_bitonic_sort_u64, "f64": L.b200_bitonic_sort_f64}[kind]
-    _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
-              ctypes.c_void_p(_stream_ptr(stream))))
+    with _on_device(t):
+        _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
+                  ctypes.c_void_p(_stream_ptr(stream))))
     return t
 
 
@@ -140,8 +155,10 @@ def sort_pairs_(keys, values, descending: bool = False, stream=None):
     kind = _key_dtype32(keys)
     fn = (_native.lib().b200_bitonic_sort_pairs_i32 if kind == "i32"
           else _native.lib().b200_bitonic_sort_pairs_u32)
-    _check(fn(ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
-              keys.numel(), int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
+    _same_device(keys, values)
+    with _on_device(keys):
+        _check(fn(ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(values.data_ptr()),
+                  keys.numel(), int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
     return keys, values
 
 
@@ -152,9 +169,11 @@ def sort_planes_(hi, lo, descending: bool = False, stream=None):
     _check_tensor(lo)
     if hi.element_size() != 4 or lo.element_size() != 4 or hi.numel() != lo.numel():
         raise ConfigError("hi and lo must be 32-bit tensors of equal length")
-    _check(_native.lib().b200_bitonic_sort_u64_planes(
-        ctypes.c_void_p(hi.data_ptr()), ctypes.c_void_p(lo.data_ptr()), hi.numel(),
-        int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
+    _same_device(hi, lo)
+    with _on_device(hi):
+        _check(_native.lib().b200_bitonic_sort_u64_planes(
+            ctypes.c_void_p(hi.data_ptr()), ctypes.c_void_p(lo.data_ptr()), hi.numel(),
+            int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
     return hi, lo
 
 
@@ -180,8 +199,9 @@ def sort_padded_(t, descending: bool = False, stream=None):
     kind = _key_dtype32(t)
     fn = (_native.lib().b200_bitonic_sort_padded_i32 if kind == "i32"
           else _native.lib().b200_bitonic_sort_padded_u32)
-    _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
-              ctypes.c_void_p(_stream_ptr(stream))))
+    with _on_device(t):
+        _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
+                  ctypes.c_void_p(_stream_ptr(stream))))
     return t
 
 
@@ -193,8 +213,9 @@ def sort_batched_(t, n_per_array: int, descending: bool = False, stream=None):
     kind = _key_dtype32(t)
     fn = (_native.lib().b200_bitonic_sort_i32_batched if kind == "i32"
           else _native.lib().b200_bitonic_sort_u32_batched)
-    _check(fn(ctypes.c_void_p(t.data_ptr()), n_per_array, t.numel() // n_per_array,
-              int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
+    with _on_device(t):
+        _check(fn(ctypes.c_void_p(t.data_ptr()), n_per_array, t.numel() // n_per_array,
+                  int(bool(descending)), ctypes.c_void_p(_stream_ptr(stream))))
     return t
 
 
@@ -226,9 +247,10 @@ def run_pass_(t, pass_index: int, n_per_array: Optional[int] = None,
     """Run a single pass of the plan on uint32 keys (profiling aid)."""
     _check_tensor(t)
     n = n_per_array or t.numel()
-    _check(_native.lib().b200_bitonic_run_pass_u32(
-        ctypes.c_void_p(t.data_ptr()), n, t.numel() // n, int(bool(descending)),
-        int(pass_index), ctypes.c_void_p(_stream_ptr(stream))))
+    with _on_device(t):
+        _check(_native.lib().b200_bitonic_run_pass_u32(
+            ctypes.c_void_p(t.data_ptr()), n, t.numel() // n, int(bool(descending)),
+            int(pass_index), ctypes.c_void_p(_stream_ptr(stream))))
     return t
 
 
@@ -242,10 +264,12 @@ def merge_split_(local, partner, out, keep_high: bool, key_xor: int = 0,
     m = local.numel()
     if partner.numel() != m or out.numel() != m:
         raise ConfigError("local, partner and out must have the same length")
-    _check(_native.lib().b200_bitonic_merge_split_u32(
-        ctypes.c_void_p(local.data_ptr()), ctypes.c_void_p(partner.data_ptr()), m,
-        int(bool(keep_high)), ctypes.c_uint32(key_xor & 0xFFFFFFFF),
-        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))))
+    _same_device(local, out)  # partner may live on a peer device (read over NVLink)
+    with _on_device(out):
+        _check(_native.lib().b200_bitonic_merge_split_u32(
+            ctypes.c_void_p(local.data_ptr()), ctypes.c_void_p(partner.data_ptr()), m,
+            int(bool(keep_high)), ctypes.c_uint32(key_xor & 0xFFFFFFFF),
+            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))))
     return out
 
 
@@ -256,10 +280,11 @@ def merge_(a, b, out, key_xor: int = 0, stream=None):
         _check_tensor(x)
     if out.numel() != a.numel() + b.numel():
         raise ConfigError("out must hold a.numel() + b.numel() keys")
-    _check(_native.lib().b200_bitonic_merge_u32(
-        ctypes.c_void_p(a.data_ptr()), a.numel(), ctypes.c_void_p(b.data_ptr()), b.numel(),
-        ctypes.c_uint32(key_xor & 0xFFFFFFFF), ctypes.c_void_p(out.data_ptr()),
-        ctypes.c_void_p(_stream_ptr(stream))))
+    with _on_device(out):
+        _check(_native.lib().b200_bitonic_merge_u32(
+            ctypes.c_void_p(a.data_ptr()), a.numel(), ctypes.c_void_p(b.data_ptr()), b.numel(),
+            ctypes.c_uint32(key_xor & 0xFFFFFFFF), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(_stream_ptr(stream))))
     return out
 
 
