@@ -363,17 +363,18 @@ struct Layout {
   // engine.cpp:16-22), so equal keys keep their payloads in place -- the
   // reference network's own payload order.
   template <int B>
-  __device__ __forceinline__ static void ce_kv(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+  __device__ __forceinline__ static void ce_kv(uint32_t (&v)[NR], uint32_t (&w)[NR],
+                                               FmaSplit fs) {
     constexpr int q = qof(B);
     static_assert(q >= 0, "CE bit must be a register bit");
 #pragma unroll
     for (int e = 0; e < NR; ++e) {
       if (!(e & (1 << q))) {
         const int f = e | (1 << q);
+        const int idx = (e & ((1 << q) - 1)) | ((e >> (q + 1)) << q);
         const uint32_t x = v[e], y = v[f];
         const bool sw = x > y;
-        v[e] = min(x, y);
-        v[f] = max(x, y);
+        mm<B200_FMA_NUM, B200_FMA_DEN>(idx, x, y, v[e], v[f], fs);
         const uint32_t a = w[e], b = w[f];
         w[e] = sw ? b : a;
         w[f] = sw ? a : b;
@@ -381,7 +382,8 @@ struct Layout {
     }
   }
   template <int B, int D>
-  __device__ __forceinline__ static void ce_dir_kv(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+  __device__ __forceinline__ static void ce_dir_kv(uint32_t (&v)[NR], uint32_t (&w)[NR],
+                                                   FmaSplit fs) {
     constexpr int q = qof(B);
     constexpr int qd = qof(D);
     static_assert(q >= 0 && qd >= 0, "CE and direction bits must be register bits");
@@ -389,11 +391,14 @@ struct Layout {
     for (int e = 0; e < NR; ++e) {
       if (!(e & (1 << q))) {
         const int f = e | (1 << q);
+        const int idx = (e & ((1 << q) - 1)) | ((e >> (q + 1)) << q);
         const uint32_t x = v[e], y = v[f];
         const bool desc = (e >> qd) & 1;
         const bool sw = desc ? (x < y) : (x > y);
-        v[e] = desc ? max(x, y) : min(x, y);
-        v[f] = desc ? min(x, y) : max(x, y);
+        uint32_t lo, hi;
+        mm<B200_FMA_NUM, B200_FMA_DEN>(idx, x, y, lo, hi, fs);
+        v[e] = desc ? hi : lo;
+        v[f] = desc ? lo : hi;
         const uint32_t a = w[e], b = w[f];
         w[e] = sw ? b : a;
         w[f] = sw ? a : b;
@@ -403,20 +408,23 @@ struct Layout {
   // 64-bit keys held as (hi word in v, lo word in w): lexicographic CE,
   // swap only when strictly out of order.
   template <int B>
-  __device__ __forceinline__ static void ce_k64(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+  __device__ __forceinline__ static void ce_k64(uint32_t (&v)[NR], uint32_t (&w)[NR],
+                                                FmaSplit fs) {
     constexpr int q = qof(B);
     static_assert(q >= 0, "CE bit must be a register bit");
 #pragma unroll
     for (int e = 0; e < NR; ++e) {
       if (!(e & (1 << q))) {
         const int f = e | (1 << q);
+        const int idx = (e & ((1 << q) - 1)) | ((e >> (q + 1)) << q);
         // x > y implies hi(x) >= hi(y): the high words are a plain min/max,
         // only the low words follow the 64-bit predicate.
         const uint64_t x = ((uint64_t)v[e] << 32) | w[e];
         const uint64_t y = ((uint64_t)v[f] << 32) | w[f];
         const bool sw = x > y;
         const uint32_t a = w[e], b = w[f];
-        const uint32_t h0 = min(v[e], v[f]), h1 = max(v[e], v[f]);
+        uint32_t h0, h1;
+        mm<B200_FMA_NUM, B200_FMA_DEN>(idx, v[e], v[f], h0, h1, fs);
         v[e] = h0;
         v[f] = h1;
         w[e] = sw ? b : a;
@@ -425,7 +433,8 @@ struct Layout {
     }
   }
   template <int B, int D>
-  __device__ __forceinline__ static void ce_dir_k64(uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+  __device__ __forceinline__ static void ce_dir_k64(uint32_t (&v)[NR], uint32_t (&w)[NR],
+                                                    FmaSplit fs) {
     constexpr int q = qof(B);
     constexpr int qd = qof(D);
     static_assert(q >= 0 && qd >= 0, "CE and direction bits must be register bits");
@@ -433,12 +442,14 @@ struct Layout {
     for (int e = 0; e < NR; ++e) {
       if (!(e & (1 << q))) {
         const int f = e | (1 << q);
+        const int idx = (e & ((1 << q) - 1)) | ((e >> (q + 1)) << q);
         const uint64_t x = ((uint64_t)v[e] << 32) | w[e];
         const uint64_t y = ((uint64_t)v[f] << 32) | w[f];
         const bool desc = (e >> qd) & 1;
         const bool sw = desc ? (x < y) : (x > y);
         const uint32_t a = w[e], b = w[f];
-        const uint32_t h0 = min(v[e], v[f]), h1 = max(v[e], v[f]);
+        uint32_t h0, h1;
+        mm<B200_FMA_NUM, B200_FMA_DEN>(idx, v[e], v[f], h0, h1, fs);
         v[e] = desc ? h1 : h0;
         v[f] = desc ? h0 : h1;
         w[e] = sw ? b : a;

@@ -346,12 +346,12 @@ struct PassBody {
     constexpr int ph = S::phase(I);
     constexpr int b = S::bit(I);
     if constexpr (natural(ph) && ph != 0) {
-      if constexpr (K64) LR::template ce_dir_k64<b, ph>(v, w);
-      else if constexpr (KV) LR::template ce_dir_kv<b, ph>(v, w);
+      if constexpr (K64) LR::template ce_dir_k64<b, ph>(v, w, c.fs);
+      else if constexpr (KV) LR::template ce_dir_kv<b, ph>(v, w, c.fs);
       else LR::template ce_dir<b, ph, FN, FD>(v, c.fs);
     } else {
-      if constexpr (K64) LR::template ce_k64<b>(v, w);
-      else if constexpr (KV) LR::template ce_kv<b>(v, w);
+      if constexpr (K64) LR::template ce_k64<b>(v, w, c.fs);
+      else if constexpr (KV) LR::template ce_kv<b>(v, w, c.fs);
       else LR::template ce<b, FN, FD>(v, c.fs);
     }
   }
