@@ -66,32 +66,77 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled during the timed
+    region: NVML every ~5 ms when pynvml is importable, else nvidia-smi."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
+        self.source = None
 
-    def _run(self):
+    def _nvml_open(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+
+        def sample():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((float(sm), mx, {n for n, b in bits.items() if r & b}))
+        self._sample = sample
+        self.source = "nvml"
+
+    def _nvml(self):
+        while not self._stop.is_set():
+            self._sample()
+            self._stop.wait(0.005)
+
+    def _smi(self):
+        self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
                     ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                      "--format=csv,noheader,nounits"],
                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 7 and f[0].replace(".", "").isdigit():
+                    self.samples.append((float(f[0]), float(f[1]) if f[1].replace(".", "").isdigit()
+                                         else None,
+                                         {n for n, v in zip(self.NAMES, f[3:7])
+                                          if v.lower() == "active"}))
             except Exception:
                 pass
             self._stop.wait(0.2)
 
+    def _run(self):
+        try:
+            if self._sample is None:
+                raise RuntimeError("no NVML")
+            self._nvml()
+        except Exception:
+            if not self.samples:
+                self._smi()
+
     def __enter__(self):
+        self._sample = None
+        try:  # open NVML and take the first sample before the timed region
+            self._nvml_open()
+            self._sample()
+        except Exception:
+            self._sample = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -100,20 +145,22 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if self._sample is not None:
+            try:
+                self._sample()  # and the last one right after it
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = sorted(x[0] for x in self.samples)
+        mx = max((x[1] for x in self.samples if x[1]), default=None)
         reasons = set()
-        for s in self.samples:
-            for n, v in zip(names, s[3:7]):
-                if v.strip().lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        for x in self.samples:
+            reasons |= x[2]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "sm_min_mhz": sm[0],
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": self.source}
 
 
 def dist_env():
