@@ -59,6 +59,7 @@ b200::PlanOptions plan_options() {
   if (const char* e = std::getenv("B200_BITONIC_REGBITS")) o.regbits = std::atoi(e);
   if (const char* e = std::getenv("B200_BITONIC_PLANNER")) o.dp = std::strcmp(e, "greedy") != 0;
   if (const char* e = std::getenv("B200_BITONIC_TILE_REGBITS")) o.tile_regbits = std::atoi(e);
+  if (const char* e = std::getenv("B200_BITONIC_CMERGE")) o.cmerge = std::atoi(e);
   return o;
 }
 
@@ -211,19 +212,19 @@ std::mutex g_plan_mu;
 struct PlanKey {
   int k;
   uint64_t batch;
-  int cmax, cmin, lrun, min_ctas, regbits, tile_regbits;
+  int cmax, cmin, lrun, min_ctas, regbits, tile_regbits, cmerge;
   bool dp, kv;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
            lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp &&
-           kv == o.kv && tile_regbits == o.tile_regbits;
+           kv == o.kv && tile_regbits == o.tile_regbits && cmerge == o.cmerge;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
   const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.tile_regbits,
-                    o.dp, o.kv};
+                    o.cmerge, o.dp, o.kv};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;
@@ -248,7 +249,7 @@ struct GraphKey {
   const void* p1;
   uint64_t n, batch;
   uint32_t kx;
-  int cmax, cmin, lrun, regbits, tile_regbits, dp, generic, pdl;
+  int cmax, cmin, lrun, regbits, tile_regbits, cmerge, dp, generic, pdl;
   bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 struct GraphEntry {
@@ -287,6 +288,7 @@ GraphKey make_key(int kind, const void* p0, const void* p1, uint64_t n, uint64_t
   key.lrun = o.lrun;
   key.regbits = o.regbits;
   key.tile_regbits = o.tile_regbits;
+  key.cmerge = o.cmerge;
   key.dp = o.dp;
   key.generic = g_force_generic.load();
   key.pdl = g_pdl.load();

@@ -131,6 +131,7 @@ struct PlanOptions {
   int tile_regbits = 0;  // override for the tile-sort pass only (0 = same)
   bool dp = true;  // cost-model planner (false: greedy packing)
   bool kv = false; // key-value plan: 16 pairs per thread, 2^12 / 2^13 tiles
+  int cmerge = 0;  // merge-pass coset size when it differs from the tile (0 = auto)
   double trip_cost = 0.10;  // extra cost of a shared-memory round trip, in passes
 };
 
@@ -213,6 +214,18 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   if (opt.tile_regbits > 0 && !opt.kv) plan.front().R = opt.tile_regbits;
   if (k <= C) return plan;
 
+  // Merge passes may use larger cosets than the tile sort: the tile sort is
+  // ALU-bound (smaller tiles do fewer steps per key), the merge passes are
+  // HBM-bound (larger cosets need fewer passes).
+  // Measured on B200 (13-bit tile + 14-bit merges vs 13/13): 2^26 2.50 vs
+  // 2.57 ms, 2^28 equal, 2^30 54.4 vs 56.6 ms; 2^24 prefers 13/13.
+  const int CT = C;
+  int cm = opt.cmerge;
+  if (cm == 0 && opt.cmin != opt.cmax && k >= 26) cm = 14;
+  if (cm > C && cm <= 15 && cm <= kt && !opt.kv && batch == 1) {
+    C = cm;
+    R = opt.regbits > 0 ? opt.regbits : 5;
+  }
   const int lrun = opt.lrun;
   auto push_tail_head = [&](int p, int b, int h) {
     PlanPass m;
@@ -289,8 +302,8 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
       memo = bc;
       return bc;
     };
-    solve(C + 1, C);
-    int p = C + 1, b = C;
+    solve(CT + 1, CT);
+    int p = CT + 1, b = CT;
     while (p <= k) {
       const int ch = choice[(size_t)p * K + b];
       if (b < C) {
@@ -310,8 +323,8 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     return plan;
   }
 
-  int p = C + 1;  // current phase
-  int b = C;      // next step bit of phase p (steps run b, b-1, ..., 0)
+  int p = CT + 1;  // current phase
+  int b = CT;      // next step bit of phase p (steps run b, b-1, ..., 0)
   while (p <= k) {
     if (b < C) {
       // Tail of phase p fits in the low bits: fuse the head of phase p+1.
