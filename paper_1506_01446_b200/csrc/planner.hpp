@@ -222,7 +222,10 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   const int CT = C;
   int cm = opt.cmerge;
   if (cm == 0 && opt.cmin != opt.cmax && k >= 26) cm = 14;
-  if (cm > C && cm <= 15 && cm <= kt && !opt.kv && batch == 1) {
+  // (cm <= C + 2: the first merge state, phase C+1 from bit C, must have its
+  // direction bit at or above local bit cm-1 -- see the tail-only / tail+head
+  // rules in the DP below.)
+  if (cm > C && cm <= C + 2 && cm <= 15 && cm <= kt && !opt.kv && batch == 1) {
     C = cm;
     R = opt.regbits > 0 ? opt.regbits : 5;
   }
@@ -278,11 +281,17 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
       double bc = 1e30;
       int bch = 0;
       if (b < C) {
-        const double t0 = cost_of(b, -1) + solve(p + 1, p);
-        bc = t0;
-        bch = 0;
+        // A tail-only pass takes phase p's direction as CTA-uniform: valid
+        // only when bit p lies above the coset (p >= C; after a smaller tile
+        // sort, p < C happens and the tail must be fused with a head).
+        if (p >= C) {
+          bc = cost_of(b, -1) + solve(p + 1, p);
+          bch = 0;
+        }
         const int h = C - (b + 1);
-        if (p < k && b + 1 >= lrun && h >= 1) {
+        // tail+head: phase p's direction bit must be the coset's top local
+        // bit C-1 (p >= C-1), which also keeps the head above the tail
+        if (p < k && p >= C - 1 && b + 1 >= lrun && h >= 1) {
           const double t1 = cost_of(b, b + 1) + solve(p + 1, p - h);
           if (t1 < bc) {
             bc = t1;
@@ -330,7 +339,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
       // Tail of phase p fits in the low bits: fuse the head of phase p+1.
       const int low = (b + 1 > lrun) ? b + 1 : lrun;
       int h = C - low;
-      if (p == k) h = 0;
+      if (p == k && p >= C) h = 0;
       push_tail_head(p, b, h > 0 ? h : 0);
       if (h > 0) {
         b = p - h;  // next step bit of phase p+1
