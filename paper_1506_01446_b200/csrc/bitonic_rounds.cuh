@@ -162,11 +162,24 @@ struct Rounds {
   }
 };
 
+// Two layouts of the same tile whose warp bits (thread bits 5 and up) sit on
+// the same local bits give every warp the same set of keys: a re-partition
+// between them only moves keys inside each warp's own shared-memory
+// addresses, so a warp barrier suffices (no CTA barrier).
+template <class LA, class LB>
+constexpr bool same_warp_bits() {
+  static_assert(LA::NT == LB::NT, "layouts of different thread counts");
+  for (int i = 5; i < LA::NT; ++i)
+    if (LA::tpos(i) != LB::tpos(i)) return false;
+  return true;
+}
+
 // ---- layouts ---------------------------------------------------------------
 template <int C, uint32_t RM>
 struct Layout {
   static constexpr int R = popc(RM);
   static constexpr int NR = 1 << R;
+  static constexpr int NT = C - R;  // thread bits
   // position of the i-th register bit / i-th thread bit
   static constexpr int rpos(int i) {
     int k = -1;

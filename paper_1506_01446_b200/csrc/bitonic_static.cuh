@@ -479,7 +479,11 @@ struct PassBody {
       if constexpr (r > 0) {
         L<r - 1>::sts(sm, v);
         if constexpr (KV) L<r - 1>::sts(sm + TW, w);
-        __syncthreads();
+        if constexpr (same_warp_bits<L<r - 1>, L<r>>()) {
+          __syncwarp();
+        } else {
+          __syncthreads();
+        }
         L<r>::lds(sm, v);
         if constexpr (KV) L<r>::lds(sm + TW, w);
       }
