@@ -122,7 +122,10 @@ int b200_bitonic_release_scratch(void);
  * the keys are copied into a stream-ordered scratch buffer of bit_ceil(n)
  * keys padded with the order's maximum (INT32_MAX for ascending int32, as
  * pad_to_pow2 does), sorted, and the first n keys are copied back.  Powers
- * of two sort in place with no allocation. */
+ * of two sort in place with no allocation.  From 2^20 keys, lengths up to
+ * 1.5 x a power of two 2^j sort the 2^j-key prefix in place, the rest
+ * recursively, and merge the two runs through a scratch buffer (same
+ * result, about 1.5 instead of 2.2 sorts' work). */
 int b200_bitonic_sort_padded_u32(uint32_t* d_keys, uint64_t n, int descending,
                                  b200_stream_t stream);
 int b200_bitonic_sort_padded_i32(int32_t* d_keys, uint64_t n, int descending,

@@ -540,11 +540,36 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
     return fail(B200_CONFIG, "descending must be 0 or 1");
   }
   if (n == 1) return B200_OK;
-  if (is_pow2(n) && (reinterpret_cast<uintptr_t>(d_keys) & 15u) == 0) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(d_keys) & 15u) == 0;
+  if (is_pow2(n) && aligned) {
     return sort_impl(d_keys, n, 1, descending, key_xor, s);
   }
   uint64_t m = 2;
   while (m < n) m <<= 1;
+  if (aligned && n >= (uint64_t{1} << 20) && n - m / 2 <= m / 4) {
+    // Just above a power of two, padding would double the work: sort the
+    // 2^j-key prefix in place, the r-key rest recursively (padded), and merge
+    // the two runs (merge path) through one scratch buffer.  Same result as
+    // pad + sort + truncate, ~1.5 instead of ~2.2 sorts of 2^j keys.
+    const uint64_t h = m / 2, r = n - h;
+    int rc = sort_impl(d_keys, h, 1, descending, key_xor, s);
+    if (rc == B200_OK) rc = padded_impl(d_keys + h, r, descending, key_xor, s);
+    if (rc != B200_OK) return rc;
+    const uint32_t kx = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+    const uint64_t tiles = (n + b200::kMergeTile - 1) / b200::kMergeTile;
+    uint32_t* out = nullptr;
+    uint64_t* cor = nullptr;
+    B200_CUDA_TRY(scratch_alloc(&out, n * 4, s));
+    B200_CUDA_TRY(scratch_alloc(&cor, (tiles + 1) * sizeof(uint64_t), s));
+    rc = merge_window_impl(d_keys, h, d_keys + h, r, 0, n, kx, out, cor, s);
+    if (rc == B200_OK) {
+      cudaError_t e = cudaMemcpyAsync(d_keys, out, n * 4, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "copy back");
+    }
+    cudaFreeAsync(cor, s);
+    cudaFreeAsync(out, s);
+    return rc;
+  }
   // padding = the largest key in the sort's order (sorts last, discarded)
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
   const uint32_t pad = ~gmask;
