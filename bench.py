@@ -437,14 +437,19 @@ def main():
     batched = args.batched
     if world > 1:
         from paper_1506_01446_b200 import dist as bdist
-        ops = bdist.cuda_ops()
+        exchange = os.environ.get("B200_BITONIC_EXCHANGE", "peer")
 
         def sort_step():
-            bdist.partitioned_sort_(work, ops=ops)
+            bdist.partitioned_sort_(work, exchange=exchange)
         plan = b200.plan(n)
+        # local sort + one fused merge-split (partition + merge kernels) per
+        # network step (the two shard copies are memcpys, not kernels)
         launches_per_step = len(plan) + 2 * len(bdist.network_steps(world))
         workload = (f"{world}x2^{args.log2n} random uint32 keys, one array partitioned "
-                    f"over {world} GPUs (local sort + NCCL merge-split network)")
+                    f"over {world} GPUs (local sort + bitonic merge-split network; "
+                    f"exchange={exchange}: "
+                    + ("partner shard read over CUDA IPC peer memory inside the merge "
+                       "kernel" if exchange == "peer" else "NCCL send/recv") + ")")
     elif batched:
         def sort_step():
             b200.sort_batched_(work, batched)

@@ -169,6 +169,25 @@ int b200_bitonic_merge_u32(const uint32_t* a, uint64_t la, const uint32_t* b,
                            uint64_t lb, uint32_t key_xor, uint32_t* out,
                            b200_stream_t stream);
 
+/* ---- cross-process peer memory (one process per GPU) ---------------------
+ * The fused merge-split of the multi-process partitioned sort reads the
+ * partner rank's shard directly over NVLink: each rank allocates its shard
+ * buffers with b200_bitonic_ipc_alloc, exchanges the 64-byte handles (any
+ * host transport, e.g. torch.distributed), and maps the partner's buffers
+ * with b200_bitonic_ipc_open; b200_bitonic_merge_split_u32 then takes the
+ * mapped pointer as `partner`.  Handles name whole allocations (offset 0). */
+typedef struct {
+  unsigned char bytes[64];
+} b200_ipc_handle;
+
+int b200_bitonic_ipc_alloc(uint64_t bytes, void** d_ptr, b200_ipc_handle* handle);
+int b200_bitonic_ipc_free(void* d_ptr);
+int b200_bitonic_ipc_open(const b200_ipc_handle* handle, void** d_ptr);
+int b200_bitonic_ipc_close(void* d_ptr);
+/* Stream-ordered device-to-device copy (moves a shard into / out of the
+ * IPC buffers). */
+int b200_bitonic_copy(void* dst, const void* src, uint64_t bytes, b200_stream_t stream);
+
 /* ---- plan introspection (host only, no GPU needed) ----------------------
  * One entry per kernel launch of the sort of `batch` arrays of n keys. */
 typedef struct {

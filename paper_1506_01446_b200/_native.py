@@ -28,6 +28,11 @@ EXPORTED = (
     "b200_bitonic_sort_f64",
     "b200_bitonic_sort_u64_planes",
     "b200_bitonic_release_scratch",
+    "b200_bitonic_ipc_alloc",
+    "b200_bitonic_ipc_free",
+    "b200_bitonic_ipc_open",
+    "b200_bitonic_ipc_close",
+    "b200_bitonic_copy",
     "b200_bitonic_sort_padded_u32",
     "b200_bitonic_sort_padded_i32",
     "b200_bitonic_sort_host_i32",
@@ -42,6 +47,10 @@ EXPORTED = (
     "b200_bitonic_last_error",
     "b200_bitonic_version",
 )
+
+
+class IpcHandle(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_ubyte * 64)]
 
 
 class PassInfo(ctypes.Structure):

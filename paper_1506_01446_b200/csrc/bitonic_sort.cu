@@ -954,6 +954,48 @@ int b200_bitonic_merge_split_u32(const uint32_t* local, const uint32_t* partner,
   return rc;
 }
 
+int b200_bitonic_ipc_alloc(uint64_t bytes, void** d_ptr, b200_ipc_handle* handle) {
+  if (!d_ptr || !handle || bytes == 0) return fail(B200_CONFIG, "bad ipc_alloc arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(b200_ipc_handle), "handle size");
+  B200_CUDA_TRY(cudaMalloc(d_ptr, bytes));
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, *d_ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*d_ptr);
+    *d_ptr = nullptr;
+    return cuda_fail(e, "cudaIpcGetMemHandle");
+  }
+  std::memset(handle, 0, sizeof(*handle));
+  std::memcpy(handle->bytes, &h, sizeof(h));
+  return B200_OK;
+}
+
+int b200_bitonic_ipc_free(void* d_ptr) {
+  if (d_ptr) B200_CUDA_TRY(cudaFree(d_ptr));
+  return B200_OK;
+}
+
+int b200_bitonic_ipc_open(const b200_ipc_handle* handle, void** d_ptr) {
+  if (!d_ptr || !handle) return fail(B200_CONFIG, "bad ipc_open arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle->bytes, sizeof(h));
+  B200_CUDA_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return B200_OK;
+}
+
+int b200_bitonic_ipc_close(void* d_ptr) {
+  if (d_ptr) B200_CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
+  return B200_OK;
+}
+
+int b200_bitonic_copy(void* dst, const void* src, uint64_t bytes, b200_stream_t stream) {
+  if (bytes == 0) return B200_OK;
+  if (!dst || !src) return fail(B200_CONFIG, "null pointer");
+  B200_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
+                                reinterpret_cast<cudaStream_t>(stream)));
+  return B200_OK;
+}
+
 // Rank-level bitonic network over G sorted shards (block bitonic sort with
 // merge-split compare-exchanges).  Same direction rule as the reference's
 // network (schedule.cpp:58-67) applied to shard indices.

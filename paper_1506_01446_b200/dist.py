@@ -20,6 +20,15 @@ becomes a merge-split (block 0-1 principle):
    random data: the "half-shard" exchange), and each rank merges what it
    kept with what it received (``merge_``, a merge-path kernel).  The
    ``exchange="full"`` mode swaps whole shards instead (NCCL baseline).
+4. ``exchange="peer"`` (the default on CUDA with the NCCL backend) fuses the
+   exchange into the merge: every rank keeps its shard in two buffers that
+   are shared with the other processes through CUDA IPC
+   (``b200_bitonic_ipc_*``), and each merge-split step is ONE kernel that
+   reads the partner's shard straight out of the partner GPU's memory over
+   NVLink/NVSwitch -- only the part of it that lands in this rank's output
+   window, ~m/2 keys on random data -- while it writes the merged output
+   locally.  Two host barriers per step order the steps (partner's shard
+   final before the read; read done before the buffer is reused).
 
 Afterwards rank r holds global sorted positions [r*m, (r+1)*m).
 
@@ -81,6 +90,106 @@ def p2p_exchange(send, recv, partner, group):
            dist.P2POp(dist.irecv, _as_wire(recv), partner, group)]
     for req in dist.batch_isend_irecv(ops):
         req.wait()
+
+
+class PeerShards:
+    """Two shard buffers per rank allocated for CUDA IPC, and every rank's
+    buffers mapped into this process (the fused peer-memory exchange)."""
+
+    def __init__(self, m: int, itemsize: int, group, rank: int, world: int):
+        import ctypes
+        from . import _native, _check
+        self._lib = _native.lib()
+        self._check = _check
+        self.bytes = m * itemsize
+        handles, self.local = [], []
+        for _ in range(2):
+            ptr, h = ctypes.c_void_p(), _native.IpcHandle()
+            _check(self._lib.b200_bitonic_ipc_alloc(self.bytes, ctypes.byref(ptr),
+                                                    ctypes.byref(h)))
+            self.local.append(ptr.value)
+            handles.append(bytes(h.bytes))
+        everyone = [None] * world
+        dist.all_gather_object(everyone, handles, group=group)
+        self.ptrs = []  # ptrs[r][i]: rank r's buffer i, mapped here
+        self._opened = []
+        for r in range(world):
+            if r == rank:
+                self.ptrs.append(list(self.local))
+                continue
+            row = []
+            for hb in everyone[r]:
+                ptr, h = ctypes.c_void_p(), _native.IpcHandle()
+                ctypes.memmove(h.bytes, hb, len(hb))
+                _check(self._lib.b200_bitonic_ipc_open(ctypes.byref(h), ctypes.byref(ptr)))
+                row.append(ptr.value)
+                self._opened.append(ptr.value)
+            self.ptrs.append(row)
+
+    def close(self) -> None:
+        import ctypes
+        for p in self._opened:
+            self._lib.b200_bitonic_ipc_close(ctypes.c_void_p(p))
+        for p in self.local:
+            self._lib.b200_bitonic_ipc_free(ctypes.c_void_p(p))
+        self._opened, self.local = [], []
+
+
+_PEER_CACHE: dict = {}
+
+
+def release_peer_buffers() -> None:
+    """Unmap and free the cached IPC shard buffers (all ranks should call it
+    together, after their last partitioned sort)."""
+    for bufs in _PEER_CACHE.values():
+        bufs.close()
+    _PEER_CACHE.clear()
+
+
+def _peer_shards(m, itemsize, group, rank, world, device):
+    key = (m, itemsize, id(group), rank, world, device.index)
+    bufs = _PEER_CACHE.get(key)
+    if bufs is None:  # collective: every rank reaches this on its first call
+        bufs = PeerShards(m, itemsize, group, rank, world)
+        _PEER_CACHE[key] = bufs
+    return bufs
+
+
+def _peer_partitioned_sort(shard, descending, group, rank, world, stats):
+    """Local sort, then every merge-split step as one kernel reading the
+    partner's shard through CUDA IPC peer memory."""
+    import ctypes
+    from . import _native, _check, _stream_ptr
+    lib = _native.lib()
+    m = shard.numel()
+    kx = key_xor_for(shard.dtype, descending)
+    with torch.cuda.device(shard.device):
+        stream = torch.cuda.current_stream(shard.device)
+        sp = ctypes.c_void_p(_stream_ptr(stream))
+        bufs = _peer_shards(m, shard.element_size(), group, rank, world, shard.device)
+        cur = 0
+        _check(lib.b200_bitonic_copy(ctypes.c_void_p(bufs.local[cur]),
+                                     ctypes.c_void_p(shard.data_ptr()), bufs.bytes, sp))
+        sort_fn = lib.b200_bitonic_sort_i32 if shard.dtype == torch.int32 \
+            else lib.b200_bitonic_sort_u32
+        _check(sort_fn(ctypes.c_void_p(bufs.local[cur]), m, int(bool(descending)), sp))
+        for q, s in network_steps(world):
+            partner, keep_high = step_role(rank, q, s)
+            stream.synchronize()
+            dist.barrier(group)  # every rank's current shard is final
+            _check(lib.b200_bitonic_merge_split_u32(
+                ctypes.c_void_p(bufs.local[cur]), ctypes.c_void_p(bufs.ptrs[partner][cur]),
+                m, int(keep_high), ctypes.c_uint32(kx & 0xFFFFFFFF),
+                ctypes.c_void_p(bufs.local[cur ^ 1]), sp))
+            stream.synchronize()
+            dist.barrier(group)  # the partner has finished reading our shard
+            cur ^= 1
+        _check(lib.b200_bitonic_copy(ctypes.c_void_p(shard.data_ptr()),
+                                     ctypes.c_void_p(bufs.local[cur]), bufs.bytes, sp))
+    if stats is not None:
+        stats["exchange"] = "peer"
+        stats["steps"] = len(network_steps(world))
+    return shard
 
 
 def cuda_ops() -> Ops:
@@ -158,25 +267,32 @@ def _half_merge_split(cur, out, partner, keep_high, kx, group, ops, s):
 
 
 def partitioned_sort_(shard: torch.Tensor, descending: bool = False, group=None,
-                      ops: Ops | None = None, exchange: str = "half",
+                      ops: Ops | None = None, exchange: str | None = None,
                       sample_stride: int = 4096, stats: dict | None = None,
                       rank: int | None = None, world: int | None = None) -> torch.Tensor:
     """Sort the distributed array whose slice ``shard`` this rank owns.
 
     All ranks must pass equal-length shards of the same dtype (int32 or
     uint32).  In place: ``shard`` receives this rank's slice of the result.
-    ``exchange``: "half" (only the keys the partner keeps cross the link) or
-    "full" (whole shards).  ``stats`` (optional dict) receives the number of
+    ``exchange``: "peer" (one fused kernel per step reads the partner's shard
+    over CUDA IPC peer memory; the default with NCCL on CUDA), "half" (NCCL
+    send/recv of only the keys the partner keeps, then a merge) or "full"
+    (whole shards).  ``stats`` (optional dict) receives the number of
     keys this rank sent per step.  ``rank``/``world`` override the process
     group's (in-process emulation of the ranks in tests).
     """
-    if exchange not in ("half", "full"):
-        raise ValueError("exchange must be 'half' or 'full'")
-    ops = ops or cuda_ops()
+    if exchange is None:
+        exchange = ("peer" if shard.is_cuda and dist.is_initialized()
+                    and dist.get_backend(group) == "nccl" and ops is None else "half")
+    if exchange not in ("half", "full", "peer"):
+        raise ValueError("exchange must be 'half', 'full' or 'peer'")
     if world is None:
         world = dist.get_world_size(group) if dist.is_initialized() else 1
     if rank is None:
         rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if exchange == "peer" and world > 1:
+        return _peer_partitioned_sort(shard, descending, group, rank, world, stats)
+    ops = ops or cuda_ops()
     ops.local_sort(shard, descending)
     if world == 1:
         return shard
