@@ -16,6 +16,8 @@
 
 #include <cstdint>
 #include <span>
+#include <utility>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -83,6 +85,48 @@ inline void sort_device_batched(std::uint32_t* d_keys, std::uint64_t n_per_array
                                 b200_stream_t stream = nullptr) {
   check(b200_bitonic_sort_u32_batched(d_keys, n_per_array, batch, ascending ? 0 : 1,
                                       stream));
+}
+
+// Counterparts of bitonic::Counters / ExecutionResult (engine.hpp:55-75),
+// same field names, so call sites reading r.keys and r.counters compile
+// unchanged.  The counters are the GPU plan's, in the reference's cost model
+// (account(), engine.cpp:147-173): one launch = n reads + n writes; CEs =
+// predicted_counts (schedule.cpp:71-78).
+struct Counters {
+  std::uint64_t kernel_launches = 0;
+  std::uint64_t global_reads = 0;
+  std::uint64_t global_writes = 0;
+  std::uint64_t compare_exchanges = 0;
+  friend bool operator==(const Counters&, const Counters&) = default;
+};
+
+struct ExecutionResult {
+  std::vector<std::int32_t> keys;
+  Counters counters;
+};
+
+inline Counters counters(std::uint64_t n, std::uint64_t batch = 1) {
+  std::uint64_t c[4] = {0, 0, 0, 0};
+  check(b200_bitonic_counters(n, batch, c));
+  return Counters{c[0], c[1], c[2], c[3]};
+}
+
+// Drop-in for bitonic::execute(const LaunchPlan&, KeyArray, unsigned)
+// (engine.hpp:86-92): takes the keys by value, returns them sorted with the
+// counters.  Any plan type with the reference's `k` member is accepted (its
+// strategy and block capacity describe CPU launches and are not used: the
+// GPU runs its own plan).  Same failures: keys.size() != 2^k throws
+// invalid_size_error, workers < 1 throws config_error.
+template <class Plan>
+inline ExecutionResult execute(const Plan& plan, std::vector<std::int32_t> keys,
+                               unsigned workers) {
+  if (plan.k >= 64 || keys.size() != (std::uint64_t{1} << plan.k)) {
+    throw invalid_size_error("execute: key count does not match the plan's 2^k");
+  }
+  if (workers < 1) throw config_error("execute: workers must be >= 1");
+  sort(std::span<std::int32_t>(keys), true);
+  const std::uint64_t n = keys.size();
+  return ExecutionResult{std::move(keys), counters(n)};
 }
 
 }  // namespace bitonic::gpu

@@ -69,6 +69,22 @@ int main() {
     CHECK(u == ue);
   }
   {
+    // execute(plan, keys, workers) shape (engine.hpp:86-92, test_engine.cpp:255-269)
+    struct PlanLike {
+      unsigned k;
+    };
+    std::vector<std::int32_t> keys(1u << 12);
+    for (auto& v : keys) v = static_cast<std::int32_t>(static_cast<std::uint32_t>(rng()));
+    auto expected = keys;
+    std::sort(expected.begin(), expected.end());
+    const auto r = bitonic::gpu::execute(PlanLike{12}, keys, 4);
+    CHECK(r.keys == expected);
+    CHECK(r.counters.compare_exchanges == (std::uint64_t{1} << 11) * 78);
+    CHECK(r.counters.global_reads == r.counters.kernel_launches << 12);
+    CHECK_THROWS_AS(bitonic::gpu::execute(PlanLike{13}, keys, 4), bitonic::invalid_size_error);
+    CHECK_THROWS_AS(bitonic::gpu::execute(PlanLike{12}, keys, 0), bitonic::config_error);
+  }
+  {
     std::vector<std::int32_t> odd(6);
     CHECK_THROWS_AS(sequential_bitonic_sort(odd), bitonic::invalid_size_error);
     std::vector<std::int32_t> one(1);
