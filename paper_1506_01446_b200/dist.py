@@ -92,6 +92,10 @@ def p2p_exchange(send, recv, partner, group):
         req.wait()
 
 
+class PeerUnavailable(RuntimeError):
+    """CUDA IPC peer mappings are not available on every rank."""
+
+
 class PeerShards:
     """Two shard buffers per rank allocated for CUDA IPC, and every rank's
     buffers mapped into this process (the fused peer-memory exchange)."""
@@ -102,29 +106,43 @@ class PeerShards:
         self._lib = _native.lib()
         self._check = _check
         self.bytes = m * itemsize
-        handles, self.local = [], []
-        for _ in range(2):
-            ptr, h = ctypes.c_void_p(), _native.IpcHandle()
-            _check(self._lib.b200_bitonic_ipc_alloc(self.bytes, ctypes.byref(ptr),
-                                                    ctypes.byref(h)))
-            self.local.append(ptr.value)
-            handles.append(bytes(h.bytes))
+        handles, self.local, self._opened = [], [], []
+        self.ptrs = []  # ptrs[r][i]: rank r's buffer i, mapped here
+        err = None
+        try:
+            for _ in range(2):
+                ptr, h = ctypes.c_void_p(), _native.IpcHandle()
+                _check(self._lib.b200_bitonic_ipc_alloc(self.bytes, ctypes.byref(ptr),
+                                                        ctypes.byref(h)))
+                self.local.append(ptr.value)
+                handles.append(bytes(h.bytes))
+        except Exception as e:  # e.g. IPC not permitted in this container
+            err, handles = repr(e), []
         everyone = [None] * world
         dist.all_gather_object(everyone, handles, group=group)
-        self.ptrs = []  # ptrs[r][i]: rank r's buffer i, mapped here
-        self._opened = []
-        for r in range(world):
-            if r == rank:
-                self.ptrs.append(list(self.local))
-                continue
-            row = []
-            for hb in everyone[r]:
-                ptr, h = ctypes.c_void_p(), _native.IpcHandle()
-                ctypes.memmove(h.bytes, hb, len(hb))
-                _check(self._lib.b200_bitonic_ipc_open(ctypes.byref(h), ctypes.byref(ptr)))
-                row.append(ptr.value)
-                self._opened.append(ptr.value)
-            self.ptrs.append(row)
+        try:
+            if err is not None or any(len(x) != 2 for x in everyone):
+                raise RuntimeError(err or "a peer rank has no IPC buffers")
+            for r in range(world):
+                if r == rank:
+                    self.ptrs.append(list(self.local))
+                    continue
+                row = []
+                for hb in everyone[r]:
+                    ptr, h = ctypes.c_void_p(), _native.IpcHandle()
+                    ctypes.memmove(h.bytes, hb, len(hb))
+                    _check(self._lib.b200_bitonic_ipc_open(ctypes.byref(h), ctypes.byref(ptr)))
+                    row.append(ptr.value)
+                    self._opened.append(ptr.value)
+                self.ptrs.append(row)
+        except Exception as e:  # e.g. no peer access / IPC not permitted here
+            err = repr(e)
+        # collective verdict: every rank mapped every peer, or nobody uses them
+        oks = [None] * world
+        dist.all_gather_object(oks, err is None, group=group)
+        if not all(oks):
+            self.close()
+            raise PeerUnavailable(err or "a peer rank could not map the IPC buffers")
 
     def close(self) -> None:
         import ctypes
@@ -291,7 +309,12 @@ def partitioned_sort_(shard: torch.Tensor, descending: bool = False, group=None,
     if rank is None:
         rank = dist.get_rank(group) if dist.is_initialized() else 0
     if exchange == "peer" and world > 1:
-        return _peer_partitioned_sort(shard, descending, group, rank, world, stats)
+        try:
+            return _peer_partitioned_sort(shard, descending, group, rank, world, stats)
+        except PeerUnavailable:
+            exchange = "half"  # every rank takes this branch together
+            if stats is not None:
+                stats["peer_fallback"] = True
     ops = ops or cuda_ops()
     ops.local_sort(shard, descending)
     if world == 1:
