@@ -438,9 +438,10 @@ def main():
     if world > 1:
         from paper_1506_01446_b200 import dist as bdist
         exchange = os.environ.get("B200_BITONIC_EXCHANGE", "peer")
+        dist_stats = {}
 
         def sort_step():
-            bdist.partitioned_sort_(work, exchange=exchange)
+            bdist.partitioned_sort_(work, exchange=exchange, stats=dist_stats)
         plan = b200.plan(n)
         # local sort + one fused merge-split (partition + merge kernels) per
         # network step (the two shard copies are memcpys, not kernels)
@@ -693,7 +694,10 @@ def main():
                        "input_restore": "D2D copy before every step (outside timing)",
                        "timing": "CUDA events on the sort stream around each step; a device "
                                  "sleep before the start event keeps host launch overhead out",
-                       "passes": len(plan)},
+                       "passes": len(plan),
+                       **({"exchange": ("half (peer unavailable)"
+                                        if dist_stats.get("peer_fallback") else exchange)}
+                          if world > 1 else {})},
             "e2e": e2e, "roofline": roofline, "sort_roofline": sort_roof,
             "cpu_baseline": cpu, "clocks": sampler.summary(),
             "gpu_launches": launches_per_step * args.steps,
