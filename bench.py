@@ -74,8 +74,12 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval: float = 0.005):
+        # multi-rank steps synchronise the host several times per step: a
+        # 5 ms sampler there costs ~10 ms per step (measured), so N > 1 samples
+        # every 100 ms
         self.index = index
+        self.interval = float(os.environ.get("B200_BENCH_CLOCK_INTERVAL", interval))
         self.samples = []  # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
@@ -101,7 +105,7 @@ class ClockSampler:
     def _nvml(self):
         while not self._stop.is_set():
             self._sample()
-            self._stop.wait(0.005)
+            self._stop.wait(self.interval)
 
     def _smi(self):
         self.source = "nvidia-smi"
@@ -418,9 +422,19 @@ def main():
     world, rank, local = dist_env()
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    # Functional test hook (never a measurement): B200_BENCH_SHARED_GPU=1 runs
+    # every rank on cuda:0 with gloo, to exercise the N>1 code path on a
+    # one-GPU box.  The ranks' kernels never wait on each other (the peer
+    # exchange is ordered by host barriers).
+    shared_gpu = world > 1 and os.environ.get("B200_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
@@ -489,7 +503,8 @@ def main():
     # ---- timed region ----------------------------------------------------------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    sampler = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    sampler = ClockSampler(torch.cuda.current_device() if world == 1 else local,
+                           0.005 if world == 1 else 0.1)
     barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
