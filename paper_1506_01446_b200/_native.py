@@ -87,6 +87,16 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_sort_u32_batched.argtypes = [vp, u64, u64, i, vp]
     L.b200_bitonic_sort_i32_batched.argtypes = [vp, u64, u64, i, vp]
     L.b200_bitonic_sort_f32.argtypes = [vp, u64, i, vp]
+    L.b200_bitonic_sort_u64.argtypes = [vp, u64, i, vp]
+    L.b200_bitonic_sort_i64.argtypes = [vp, u64, i, vp]
+    L.b200_bitonic_sort_f64.argtypes = [vp, u64, i, vp]
+    L.b200_bitonic_sort_u64_planes.argtypes = [vp, vp, u64, i, vp]
+    L.b200_bitonic_release_scratch.argtypes = []
+    L.b200_bitonic_ipc_alloc.argtypes = [u64, ctypes.POINTER(vp), ctypes.POINTER(IpcHandle)]
+    L.b200_bitonic_ipc_free.argtypes = [vp]
+    L.b200_bitonic_ipc_open.argtypes = [ctypes.POINTER(IpcHandle), ctypes.POINTER(vp)]
+    L.b200_bitonic_ipc_close.argtypes = [vp]
+    L.b200_bitonic_copy.argtypes = [vp, vp, u64, vp]
     L.b200_bitonic_sort_pairs_u32.argtypes = [vp, vp, u64, i, vp]
     L.b200_bitonic_sort_pairs_i32.argtypes = [vp, vp, u64, i, vp]
     L.b200_bitonic_sort_pairs_u32_batched.argtypes = [vp, vp, u64, u64, i, vp]
@@ -103,6 +113,8 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_run_pass_u32.argtypes = [vp, u64, u64, i, i, vp]
     L.b200_bitonic_counters.argtypes = [u64, u64, ctypes.POINTER(ctypes.c_uint64)]
     L.b200_bitonic_set_tuning.argtypes = [i, i]
+    L.b200_bitonic_last_error.argtypes = []
+    L.b200_bitonic_version.argtypes = []
     L.b200_bitonic_last_error.restype = ctypes.c_char_p
     L.b200_bitonic_version.restype = ctypes.c_char_p
     for name in EXPORTED:

@@ -42,6 +42,14 @@ def test_library_exports_every_declared_symbol():
         assert getattr(L, name) is not None
 
 
+def test_every_entry_has_argtypes():
+    """ctypes would pass Python ints as 32-bit C ints without argtypes: every
+    entry taking a 64-bit length (or any argument) must declare them."""
+    L = _native.lib()
+    missing = [name for name in _native.EXPORTED if getattr(L, name).argtypes is None]
+    assert not missing, missing
+
+
 def test_library_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH],
                          capture_output=True, text=True).stdout
