@@ -183,8 +183,11 @@ def release_scratch() -> None:
 
 
 def argsort(keys, descending: bool = False, stream=None):
-    """Indices that sort ``keys`` (not modified), via the key-value network."""
+    """Indices that sort ``keys`` (not modified), via the key-value network.
+    int32 indices: up to 2^31 keys."""
     import torch
+    if keys.numel() > (1 << 31):
+        raise ConfigError("argsort returns int32 indices: at most 2^31 keys")
     k = keys.clone()
     idx = torch.arange(keys.numel(), dtype=torch.int32, device=keys.device)
     sort_pairs_(k, idx, descending=descending, stream=stream)
