@@ -165,7 +165,10 @@ def release_peer_buffers() -> None:
 
 
 def _peer_shards(m, itemsize, group, rank, world, device):
-    key = (m, itemsize, id(group), rank, world, device.index)
+    # key on the group's member ranks, not id(group): a dead group's id can be
+    # reused by a new group object
+    members = tuple(dist.get_process_group_ranks(group)) if group is not None else None
+    key = (m, itemsize, members, rank, world, device.index)
     bufs = _PEER_CACHE.get(key)
     if bufs is None:  # collective: every rank reaches this on its first call
         bufs = PeerShards(m, itemsize, group, rank, world)
