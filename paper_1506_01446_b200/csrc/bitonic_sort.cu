@@ -1,4 +1,4 @@
-// bitonic_sort.cu -- launcher, C ABI, merge-split and the partitioned sort.
+// bitonic_sort.cu -- launcher, plans, graphs, merge path and the device entries.
 //
 // Host side of the B200-native bitonic sort.  Replaces, behind the C ABI in
 // include/b200_bitonic.h, the reference's execute() (engine.cpp:175-227):
@@ -24,8 +24,9 @@
 #include "kernel_tables.hpp"
 #include "merge_split.cuh"
 #include "planner.hpp"
+#include "runtime.hpp"
 
-namespace {
+namespace b200::rt {
 
 thread_local std::string g_last_error;
 
@@ -41,12 +42,6 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(B200_CUDA_ERROR,
               std::string(what) + ": " + cudaGetErrorString(e));
 }
-
-#define B200_CUDA_TRY(expr)                        \
-  do {                                             \
-    cudaError_t _e = (expr);                       \
-    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
-  } while (0)
 
 b200::PlanOptions plan_options() {
   b200::PlanOptions o;
@@ -131,9 +126,15 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
   return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
-template <class T>
-cudaError_t scratch_alloc(T** p, size_t bytes, cudaStream_t s) {
-  return scratch_alloc(reinterpret_cast<void**>(p), bytes, s);
+
+cudaError_t trim_scratch_pools() {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (cudaMemPool_t p : g_pools) {
+    if (p == nullptr) continue;
+    cudaError_t e = cudaMemPoolTrimTo(p, 0);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 std::atomic<int> g_force_generic{0};
@@ -246,21 +247,6 @@ std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanO
 // is a single cudaGraphLaunch on the caller's stream.  Calls made while the
 // caller's stream is itself being captured launch directly (they become
 // part of the caller's graph).  B200_BITONIC_GRAPHS=0 disables this.
-struct GraphKey {
-  int dev, kind, mode, desc, k, G;
-  const void* p0;
-  const void* p1;
-  uint64_t n, batch;
-  uint32_t kx;
-  int cmax, cmin, lrun, regbits, tile_regbits, cmerge, dp, generic, pdl;
-  double trip_cost;
-  bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
-};
-struct GraphEntry {
-  GraphKey key;
-  int hits = 0;
-  cudaGraphExec_t exec = nullptr;
-};
 std::mutex g_graph_mu;
 std::vector<GraphEntry> g_graphs;
 thread_local cudaStream_t t_capture_stream[64] = {};
@@ -300,68 +286,6 @@ GraphKey make_key(int kind, const void* p0, const void* p1, uint64_t n, uint64_t
   return key;
 }
 
-// Runs fn(stream) directly, or through a cached graph once `key` repeats.
-template <class Fn>
-int run_graphed(const GraphKey& key, cudaStream_t s, Fn&& fn) {
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  if (!graphs_enabled() || cudaStreamIsCapturing(s, &st) != cudaSuccess ||
-      st != cudaStreamCaptureStatusNone) {
-    cudaGetLastError();
-    return fn(s);
-  }
-  cudaGraphExec_t exec = nullptr;
-  bool capture = false;
-  {
-    std::lock_guard<std::mutex> lk(g_graph_mu);
-    auto it = std::find_if(g_graphs.begin(), g_graphs.end(),
-                           [&](const GraphEntry& e) { return e.key == key; });
-    if (it == g_graphs.end()) {
-      if (g_graphs.size() >= 64) {
-        if (g_graphs.front().exec) cudaGraphExecDestroy(g_graphs.front().exec);
-        g_graphs.erase(g_graphs.begin());
-      }
-      GraphEntry e;
-      e.key = key;
-      e.hits = 1;
-      g_graphs.push_back(e);
-    } else {
-      exec = it->exec;
-      capture = exec == nullptr;
-      ++it->hits;
-    }
-  }
-  if (exec == nullptr && !capture) return fn(s);  // first sighting: launch directly
-  if (exec == nullptr) {
-    cudaStream_t& cs = t_capture_stream[key.dev & 63];
-    if (cs == nullptr) B200_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    B200_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    int rc = fn(cs);
-    cudaGraph_t g = nullptr;
-    cudaError_t e = cudaStreamEndCapture(cs, &g);
-    if (rc != B200_OK) {
-      if (g) cudaGraphDestroy(g);
-      return rc;
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "graph capture");
-    e = cudaGraphInstantiateWithFlags(&exec, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
-    std::lock_guard<std::mutex> lk(g_graph_mu);
-    auto it = std::find_if(g_graphs.begin(), g_graphs.end(),
-                           [&](const GraphEntry& x) { return x.key == key; });
-    if (it != g_graphs.end() && it->exec == nullptr) {
-      it->exec = exec;
-    } else {
-      // another thread won the race: launch ours once, keep theirs
-      cudaError_t le = cudaGraphLaunch(exec, s);
-      cudaGraphExecDestroy(exec);
-      return le == cudaSuccess ? B200_OK : cuda_fail(le, "graph launch");
-    }
-  }
-  B200_CUDA_TRY(cudaGraphLaunch(exec, s));
-  return B200_OK;
-}
-
 void drop_graphs() {
   std::lock_guard<std::mutex> lk(g_graph_mu);
   for (auto& e : g_graphs)
@@ -374,8 +298,7 @@ void drop_graphs() {
 // word).  d_vals: payloads (mode 1) or the lo words of 64-bit keys whose hi
 // words are d_keys (mode 2).
 int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
-              uint32_t key_xor, cudaStream_t stream, int only = -1,
-              uint32_t* d_vals = nullptr, int mode = -1) {
+              uint32_t key_xor, cudaStream_t stream, int only, uint32_t* d_vals, int mode) {
   if (mode < 0) mode = d_vals != nullptr ? 1 : 0;
   if (mode != 0 && d_vals == nullptr) return fail(B200_CONFIG, "null second array");
   if (n_per < 2 || !is_pow2(n_per)) {
@@ -596,201 +519,13 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
 }
 
 
-// ---- host-span entry: pipelined H2D / sort / D2H ----------------------------
-// The reference's entry points sort host spans (sequential_bitonic_sort,
-// engine.hpp:102-104).  Here the span is cut into G chunks: chunk j's H2D
-// copy overlaps the bitonic sort of the chunks already on the device (one
-// stream per chunk); the sorted chunks are combined by a merge-path tree
-// (the merge kernels of the multi-GPU path), and the last merge is cut into
-// output windows so each window's D2H copy overlaps the merge of the next.
-// Device buffers and streams are cached per device (retained pool memory).
-struct HostPipe {
-  static constexpr int kMaxChunks = 8;
-  bool init = false;
-  cudaStream_t h2d = nullptr, d2h = nullptr, comp[kMaxChunks] = {};
-  std::vector<cudaEvent_t> ev;
-  std::mutex mu;
-  void* block = nullptr;  // device buffers, see pipe_buffers
-  size_t cap = 0;
-};
-std::mutex g_pipe_mu;
-std::vector<HostPipe*> g_pipes;
+}  // namespace b200::rt
 
-HostPipe* host_pipe(int dev) {
-  std::lock_guard<std::mutex> lk(g_pipe_mu);
-  if ((int)g_pipes.size() <= dev) g_pipes.resize(dev + 1, nullptr);
-  if (g_pipes[dev] == nullptr) g_pipes[dev] = new HostPipe();  // lives for the process
-  return g_pipes[dev];
-}
-
-cudaError_t pipe_init(HostPipe& P) {
-  if (P.init) return cudaSuccess;
-  cudaError_t e = cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking);
-  for (int j = 0; j < HostPipe::kMaxChunks && e == cudaSuccess; ++j)
-    e = cudaStreamCreateWithFlags(&P.comp[j], cudaStreamNonBlocking);
-  while (e == cudaSuccess && P.ev.size() < 64) {
-    cudaEvent_t x;
-    e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
-    if (e == cudaSuccess) P.ev.push_back(x);
-  }
-  if (e == cudaSuccess) P.init = true;
-  return e;
-}
-
-// Chunk count: chunks of >= 2^22 keys (16 MiB), at most 8 (measured on B200
-// + PCIe 5: up to 2^22 keys one chunk wins; at 2^24, 4 chunks save ~10%).
-int pipe_chunks(uint64_t n) {
-  if (const char* e = std::getenv("B200_BITONIC_HOST_CHUNKS")) {
-    int g = std::atoi(e);
-    if (g >= 1 && g <= HostPipe::kMaxChunks && (g & (g - 1)) == 0 && n / g >= 2) return g;
-  }
-  int g = 1;
-  while (g < HostPipe::kMaxChunks && n / (uint64_t)(2 * g) >= (uint64_t{1} << 22)) g *= 2;
-  return g;
-}
-
-// Device buffers for the host entry: [A: n keys | B: n keys | coranks],
-// one allocation per device, grown on demand and kept (graphs refer to it).
-cudaError_t pipe_buffers(HostPipe& P, uint64_t n, uint64_t cor_words) {
-  const size_t need = n * 8 + cor_words * 8;
-  if (P.cap >= need) return cudaSuccess;
-  if (P.block) {
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) return e;
-    drop_graphs();  // captured pipelines refer to the old block
-    cudaFree(P.block);
-    P.block = nullptr;
-    P.cap = 0;
-  }
-  cudaError_t e = cudaMalloc(&P.block, need);
-  if (e == cudaSuccess) P.cap = need;
-  return e;
-}
-
-int host_sort(uint32_t* h, uint64_t n, int descending, uint32_t key_xor) {
-  if (n < 2 || !is_pow2(n)) {
-    return fail(B200_INVALID_SIZE,
-                "length must be a power of two >= 2, got " + std::to_string(n));
-  }
-  if (h == nullptr) return fail(B200_CONFIG, "null key pointer");
-  if (descending != 0 && descending != 1) {
-    return fail(B200_CONFIG, "descending must be 0 or 1");
-  }
-  int dev = 0;
-  B200_CUDA_TRY(cudaGetDevice(&dev));
-  HostPipe& P = *host_pipe(dev);
-  std::lock_guard<std::mutex> lk(P.mu);
-  B200_CUDA_TRY(pipe_init(P));
-  const int G = pipe_chunks(n);
-  const uint64_t c = n / G;
-  const uint32_t kx = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
-  const uint64_t cor_per_round = n / b200::kMergeTile + 2 * HostPipe::kMaxChunks + 2;
-  int rounds = 0;
-  while ((1 << rounds) < G) ++rounds;
-  B200_CUDA_TRY(pipe_buffers(P, n, cor_per_round * (rounds + 1)));
-  uint32_t* A = reinterpret_cast<uint32_t*>(P.block);
-  uint32_t* B = A + n;
-  uint64_t* cor = reinterpret_cast<uint64_t*>(B + n);
-
-  // The whole pipeline, forked from and joined back into `origin`.
-  auto pipeline = [&](cudaStream_t origin) -> int {
-    int rc = B200_OK;
-    size_t evi = 0;
-    auto dep = [&](cudaStream_t from, cudaStream_t to) {
-      if (from == to) return;
-      cudaEvent_t x = P.ev[evi++ % P.ev.size()];
-      cudaEventRecord(x, from);
-      cudaStreamWaitEvent(to, x, 0);
-    };
-    if (G == 1) {
-      cudaError_t e = cudaMemcpyAsync(A, h, n * 4, cudaMemcpyHostToDevice, origin);
-      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-      rc = sort_impl(A, n, 1, descending, key_xor, origin);
-      if (rc != B200_OK) return rc;
-      e = cudaMemcpyAsync(h, A, n * 4, cudaMemcpyDeviceToHost, origin);
-      return e == cudaSuccess ? B200_OK : cuda_fail(e, "D2H copy");
-    }
-    dep(origin, P.h2d);
-    for (int j = 0; j < G; ++j) dep(origin, P.comp[j]);
-    // 1. chunk j: H2D on the copy stream, then its sort on stream j
-    for (int j = 0; j < G && rc == B200_OK; ++j) {
-      cudaError_t e = cudaMemcpyAsync(A + j * c, h + j * c, c * 4, cudaMemcpyHostToDevice,
-                                      P.h2d);
-      if (e != cudaSuccess) {
-        rc = cuda_fail(e, "H2D copy");
-        break;
-      }
-      dep(P.h2d, P.comp[j]);
-      rc = sort_impl(A + j * c, c, 1, descending, key_xor, P.comp[j]);
-    }
-    // 2. merge tree: run r lives on stream comp[owner[r]]
-    std::vector<int> owner(G);
-    for (int j = 0; j < G; ++j) owner[j] = j;
-    uint32_t* src = A;
-    uint32_t* dst = B;
-    uint64_t len = c;
-    int runs = G, round = 0;
-    while (runs > 2 && rc == B200_OK) {
-      std::vector<int> nowner(runs / 2);
-      for (int q = 0; q < runs / 2 && rc == B200_OK; ++q) {
-        cudaStream_t sq = P.comp[owner[2 * q]];
-        dep(P.comp[owner[2 * q + 1]], sq);
-        uint64_t* cq = cor + round * cor_per_round + q * (2 * len / b200::kMergeTile + 2);
-        rc = merge_window_impl(src + 2 * q * len, len, src + (2 * q + 1) * len, len, 0,
-                               2 * len, kx, dst + 2 * q * len, cq, sq);
-        nowner[q] = owner[2 * q];
-      }
-      owner = nowner;
-      std::swap(src, dst);
-      len *= 2;
-      runs /= 2;
-      ++round;
-    }
-    // 3. last merge in output windows, each copied back as soon as it is done
-    if (rc == B200_OK) {
-      cudaStream_t sm = P.comp[owner[0]];
-      dep(P.comp[owner[1]], sm);
-      const int W = G;
-      const uint64_t ow = n / W;
-      uint64_t* cw = cor + round * cor_per_round;
-      for (int w = 0; w < W && rc == B200_OK; ++w) {
-        rc = merge_window_impl(src, len, src + len, len, w * ow, ow, kx, dst + w * ow, cw, sm);
-        if (rc != B200_OK) break;
-        dep(sm, P.d2h);
-        cudaError_t e = cudaMemcpyAsync(h + w * ow, dst + w * ow, ow * 4,
-                                        cudaMemcpyDeviceToHost, P.d2h);
-        if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
-      }
-    }
-    // join every stream back into the origin
-    dep(P.d2h, origin);
-    dep(P.h2d, origin);
-    for (int j = 0; j < G; ++j) dep(P.comp[j], origin);
-    return rc;
-  };
-
-  // Graph only page-locked spans (a pageable copy cannot be captured).
-  cudaPointerAttributes attr{};
-  const bool pinned = cudaPointerGetAttributes(&attr, h) == cudaSuccess &&
-                      attr.type == cudaMemoryTypeHost;
-  cudaGetLastError();
-  cudaStream_t s0 = P.comp[0];
-  int rc;
-  if (pinned) {
-    rc = run_graphed(make_key(1, h, P.block, n, 1, descending, key_xor, 0, G, plan_options()),
-                     s0, pipeline);
-  } else {
-    rc = pipeline(s0);
-  }
-  cudaError_t e = cudaStreamSynchronize(s0);
-  if (rc == B200_OK && e != cudaSuccess) rc = cuda_fail(e, "host sort");
-  return rc;
-}
-
-}  // namespace
+using namespace b200::rt;
 
 extern "C" {
+
+
 
 int b200_bitonic_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, uint64_t n,
                                 int descending, b200_stream_t stream) {
@@ -856,28 +591,6 @@ int b200_bitonic_sort_u64_planes(uint32_t* d_hi, uint32_t* d_lo, uint64_t n,
                    d_lo, 2);
 }
 
-int b200_bitonic_release_scratch(void) {
-  drop_graphs();
-  {
-    std::lock_guard<std::mutex> lk(g_pipe_mu);
-    for (HostPipe* hp : g_pipes) {
-      if (hp == nullptr || hp->block == nullptr) continue;
-      std::lock_guard<std::mutex> lk2(hp->mu);
-      if (hp->init) cudaStreamSynchronize(hp->comp[0]);
-      cudaFree(hp->block);
-      hp->block = nullptr;
-      hp->cap = 0;
-    }
-  }
-  std::lock_guard<std::mutex> lk(g_pool_mu);
-  for (cudaMemPool_t p : g_pools) {
-    if (p == nullptr) continue;
-    cudaError_t e = cudaMemPoolTrimTo(p, 0);
-    if (e != cudaSuccess) return cuda_fail(e, "trim scratch pool");
-  }
-  return B200_OK;
-}
-
 int b200_bitonic_sort_padded_u32(uint32_t* d_keys, uint64_t n, int descending,
                                  b200_stream_t stream) {
   return padded_impl(d_keys, n, descending, 0u, reinterpret_cast<cudaStream_t>(stream));
@@ -914,237 +627,6 @@ int b200_bitonic_sort_i32_batched(int32_t* d_keys, uint64_t n_per_array,
   return sort_impl(reinterpret_cast<uint32_t*>(d_keys), n_per_array, batch,
                    descending, 0x80000000u,
                    reinterpret_cast<cudaStream_t>(stream));
-}
-
-int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending) {
-  return host_sort(reinterpret_cast<uint32_t*>(h_keys), n, descending,
-                   0x80000000u);
-}
-
-int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending) {
-  return host_sort(h_keys, n, descending, 0u);
-}
-
-int b200_bitonic_merge_u32(const uint32_t* a, uint64_t la, const uint32_t* b,
-                           uint64_t lb, uint32_t key_xor, uint32_t* out,
-                           b200_stream_t stream) {
-  if (la + lb == 0) return B200_OK;
-  if ((la && !a) || (lb && !b) || !out) return fail(B200_CONFIG, "null pointer");
-  if ((la && out == a) || (lb && out == b)) {
-    return fail(B200_CONFIG, "out must not alias the inputs");
-  }
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const uint64_t tiles = (la + lb + b200::kMergeTile - 1) / b200::kMergeTile;
-  uint64_t* cor = nullptr;
-  B200_CUDA_TRY(scratch_alloc(&cor, (tiles + 1) * sizeof(uint64_t), s));
-  int rc = merge_window_impl(a, la, b, lb, 0, la + lb, key_xor, out, cor, s);
-  cudaFreeAsync(cor, s);
-  return rc;
-}
-
-int b200_bitonic_merge_split_u32(const uint32_t* local, const uint32_t* partner,
-                                 uint64_t m, int keep_high, uint32_t key_xor,
-                                 uint32_t* out, b200_stream_t stream) {
-  if (m < 1) return fail(B200_INVALID_SIZE, "shard must hold >= 1 key");
-  if (!local || !partner || !out) return fail(B200_CONFIG, "null pointer");
-  if (out == local || out == partner) {
-    return fail(B200_CONFIG, "out must not alias the inputs");
-  }
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const uint64_t tiles = (m + b200::kMergeTile - 1) / b200::kMergeTile;
-  uint64_t* cor = nullptr;
-  B200_CUDA_TRY(scratch_alloc(&cor, (tiles + 1) * sizeof(uint64_t), s));
-  int rc = merge_split_impl(local, partner, m, keep_high, key_xor, out, cor, s);
-  cudaFreeAsync(cor, s);
-  return rc;
-}
-
-int b200_bitonic_ipc_alloc(uint64_t bytes, void** d_ptr, b200_ipc_handle* handle) {
-  if (!d_ptr || !handle || bytes == 0) return fail(B200_CONFIG, "bad ipc_alloc arguments");
-  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(b200_ipc_handle), "handle size");
-  B200_CUDA_TRY(cudaMalloc(d_ptr, bytes));
-  cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, *d_ptr);
-  if (e != cudaSuccess) {
-    cudaFree(*d_ptr);
-    *d_ptr = nullptr;
-    return cuda_fail(e, "cudaIpcGetMemHandle");
-  }
-  std::memset(handle, 0, sizeof(*handle));
-  std::memcpy(handle->bytes, &h, sizeof(h));
-  return B200_OK;
-}
-
-int b200_bitonic_ipc_free(void* d_ptr) {
-  if (d_ptr) B200_CUDA_TRY(cudaFree(d_ptr));
-  return B200_OK;
-}
-
-int b200_bitonic_ipc_open(const b200_ipc_handle* handle, void** d_ptr) {
-  if (!d_ptr || !handle) return fail(B200_CONFIG, "bad ipc_open arguments");
-  cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle->bytes, sizeof(h));
-  B200_CUDA_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
-  return B200_OK;
-}
-
-int b200_bitonic_ipc_close(void* d_ptr) {
-  if (d_ptr) B200_CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
-  return B200_OK;
-}
-
-int b200_bitonic_copy(void* dst, const void* src, uint64_t bytes, b200_stream_t stream) {
-  if (bytes == 0) return B200_OK;
-  if (!dst || !src) return fail(B200_CONFIG, "null pointer");
-  B200_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
-                                reinterpret_cast<cudaStream_t>(stream)));
-  return B200_OK;
-}
-
-// Rank-level bitonic network over G sorted shards (block bitonic sort with
-// merge-split compare-exchanges).  Same direction rule as the reference's
-// network (schedule.cpp:58-67) applied to shard indices.
-int b200_bitonic_sort_u32_multi(uint32_t* const* d_shards, const int* devices,
-                                int ngpu, uint64_t n_total, int descending) {
-  if (ngpu != 1 && ngpu != 2 && ngpu != 4 && ngpu != 8) {
-    return fail(B200_CONFIG, "ngpu must be 1, 2, 4 or 8");
-  }
-  if (!d_shards || !devices) return fail(B200_CONFIG, "null pointer");
-  if (n_total < 2 || !is_pow2(n_total) || n_total < (uint64_t)ngpu * 2) {
-    return fail(B200_INVALID_SIZE,
-                "n_total must be a power of two >= 2*ngpu");
-  }
-  if (descending != 0 && descending != 1) {
-    return fail(B200_CONFIG, "descending must be 0 or 1");
-  }
-  const uint64_t m = n_total / ngpu;
-  const uint32_t gmask = descending ? 0xFFFFFFFFu : 0u;
-  int prev_dev = 0;
-  B200_CUDA_TRY(cudaGetDevice(&prev_dev));
-
-  // Enable peer access between distinct devices.
-  for (int r = 0; r < ngpu; ++r) {
-    for (int q = 0; q < ngpu; ++q) {
-      if (devices[r] == devices[q]) continue;
-      int can = 0;
-      B200_CUDA_TRY(cudaDeviceCanAccessPeer(&can, devices[r], devices[q]));
-      if (!can) {
-        cudaSetDevice(prev_dev);
-        return fail(B200_CONFIG, "no peer access between devices");
-      }
-      B200_CUDA_TRY(cudaSetDevice(devices[r]));
-      cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
-      if (e == cudaErrorPeerAccessAlreadyEnabled) {
-        cudaGetLastError();
-      } else if (e != cudaSuccess) {
-        cudaSetDevice(prev_dev);
-        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
-      }
-    }
-  }
-
-  std::vector<cudaStream_t> st(ngpu, nullptr);
-  std::vector<cudaEvent_t> ev(ngpu, nullptr);
-  std::vector<uint32_t*> cur(d_shards, d_shards + ngpu), tmp(ngpu, nullptr);
-  std::vector<uint32_t*> scratch(ngpu, nullptr);
-  std::vector<uint64_t*> cor(ngpu, nullptr);
-  const uint64_t tiles = (m + b200::kMergeTile - 1) / b200::kMergeTile;
-  int rc = B200_OK;
-  auto cleanup = [&]() {
-    for (int r = 0; r < ngpu; ++r) {
-      cudaSetDevice(devices[r]);
-      if (st[r]) cudaStreamSynchronize(st[r]);
-      if (scratch[r]) cudaFree(scratch[r]);
-      if (cor[r]) cudaFree(cor[r]);
-      if (ev[r]) cudaEventDestroy(ev[r]);
-      if (st[r]) cudaStreamDestroy(st[r]);
-    }
-    cudaSetDevice(prev_dev);
-  };
-#define MTRY(expr)                                   \
-  do {                                               \
-    cudaError_t _e = (expr);                         \
-    if (_e != cudaSuccess) {                         \
-      rc = cuda_fail(_e, #expr);                     \
-      cleanup();                                     \
-      return rc;                                     \
-    }                                                \
-  } while (0)
-
-  for (int r = 0; r < ngpu; ++r) {
-    MTRY(cudaSetDevice(devices[r]));
-    MTRY(cudaStreamCreateWithFlags(&st[r], cudaStreamNonBlocking));
-    MTRY(cudaEventCreateWithFlags(&ev[r], cudaEventDisableTiming));
-    if (ngpu > 1) {
-      MTRY(cudaMalloc(&scratch[r], m * 4));
-      tmp[r] = scratch[r];
-      MTRY(cudaMalloc(&cor[r], (tiles + 1) * sizeof(uint64_t)));
-    }
-  }
-  // 1. local sorts (each shard ascending in the requested order)
-  for (int r = 0; r < ngpu; ++r) {
-    MTRY(cudaSetDevice(devices[r]));
-    rc = sort_impl(cur[r], m, 1, descending, 0u, st[r]);
-    if (rc != B200_OK) {
-      std::string msg = g_last_error;
-      cleanup();
-      g_last_error = msg;
-      return rc;
-    }
-  }
-  // 2. rank-level network: phases q = 1..g, steps s = q..1
-  int g = 0;
-  while ((1 << g) < ngpu) ++g;
-  for (int q = 1; q <= g; ++q) {
-    for (int s = q; s >= 1; --s) {
-      for (int r = 0; r < ngpu; ++r) {
-        MTRY(cudaSetDevice(devices[r]));
-        MTRY(cudaEventRecord(ev[r], st[r]));
-      }
-      for (int r = 0; r < ngpu; ++r) {
-        const int partner = r ^ (1 << (s - 1));
-        MTRY(cudaSetDevice(devices[r]));
-        MTRY(cudaStreamWaitEvent(st[r], ev[partner], 0));
-        const bool ascending = ((r >> q) & 1) == 0;
-        const bool lower = r < partner;
-        const int keep_high = (lower == ascending) ? 0 : 1;
-        rc = merge_split_impl(cur[r], cur[partner], m, keep_high, gmask,
-                              tmp[r], cor[r], st[r]);
-        if (rc != B200_OK) {
-          std::string msg = g_last_error;
-          cleanup();
-          g_last_error = msg;
-          return rc;
-        }
-      }
-      // both halves of every pair must finish reading before buffers swap
-      for (int r = 0; r < ngpu; ++r) {
-        MTRY(cudaSetDevice(devices[r]));
-        MTRY(cudaEventRecord(ev[r], st[r]));
-      }
-      for (int r = 0; r < ngpu; ++r) {
-        const int partner = r ^ (1 << (s - 1));
-        MTRY(cudaSetDevice(devices[r]));
-        MTRY(cudaStreamWaitEvent(st[r], ev[partner], 0));
-      }
-      std::swap(cur, tmp);
-    }
-  }
-  // 3. results must end in the caller's buffers
-  for (int r = 0; r < ngpu; ++r) {
-    if (cur[r] != d_shards[r]) {
-      MTRY(cudaSetDevice(devices[r]));
-      MTRY(cudaMemcpyAsync(d_shards[r], cur[r], m * 4, cudaMemcpyDeviceToDevice,
-                           st[r]));
-    }
-  }
-  for (int r = 0; r < ngpu; ++r) {
-    MTRY(cudaSetDevice(devices[r]));
-    MTRY(cudaStreamSynchronize(st[r]));
-  }
-  cleanup();
-#undef MTRY
-  return B200_OK;
 }
 
 int b200_bitonic_plan(uint64_t n, uint64_t batch, b200_pass_info* out,

@@ -21,11 +21,10 @@
 
 #include <cstdint>
 
+#include "merge_consts.hpp"
+
 namespace b200 {
 
-constexpr int kMergeThreads = 256;
-constexpr int kMergeItems = 8;
-constexpr uint64_t kMergeTile = (uint64_t)kMergeThreads * kMergeItems;
 
 // Number of keys of A among the first d keys of merge(A, B) (A first on ties).
 __device__ __forceinline__ uint64_t corank_global(uint64_t d, const uint32_t* A,
