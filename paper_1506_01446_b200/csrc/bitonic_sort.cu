@@ -56,6 +56,8 @@ b200::PlanOptions plan_options() {
   if (const char* e = std::getenv("B200_BITONIC_TILE_REGBITS")) o.tile_regbits = std::atoi(e);
   if (const char* e = std::getenv("B200_BITONIC_CMERGE")) o.cmerge = std::atoi(e);
   if (const char* e = std::getenv("B200_BITONIC_TRIP_COST")) o.trip_cost = std::atof(e);
+  if (const char* e = std::getenv("B200_BITONIC_MIXED_C")) o.mixed_c = std::atoi(e) != 0;
+  if (const char* e = std::getenv("B200_BITONIC_WIDE_TAIL_COST")) o.wide_tail_cost = std::atof(e);
   return o;
 }
 
@@ -217,18 +219,21 @@ struct PlanKey {
   int cmax, cmin, lrun, min_ctas, regbits, tile_regbits, cmerge;
   bool dp, kv;
   double trip_cost;
+  bool mixed_c;
+  double wide_tail_cost;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
            lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp &&
            kv == o.kv && tile_regbits == o.tile_regbits && cmerge == o.cmerge &&
-           trip_cost == o.trip_cost;
+           trip_cost == o.trip_cost && mixed_c == o.mixed_c &&
+           wide_tail_cost == o.wide_tail_cost;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
   const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.tile_regbits,
-                    o.cmerge, o.dp, o.kv, o.trip_cost};
+                    o.cmerge, o.dp, o.kv, o.trip_cost, o.mixed_c, o.wide_tail_cost};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;
@@ -280,6 +285,8 @@ GraphKey make_key(int kind, const void* p0, const void* p1, uint64_t n, uint64_t
   key.tile_regbits = o.tile_regbits;
   key.cmerge = o.cmerge;
   key.trip_cost = o.trip_cost;
+  key.wide_tail_cost = o.wide_tail_cost;
+  key.mixed_c = o.mixed_c;
   key.dp = o.dp;
   key.generic = g_force_generic.load();
   key.pdl = g_pdl.load();

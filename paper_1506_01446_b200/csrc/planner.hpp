@@ -132,6 +132,8 @@ struct PlanOptions {
   bool dp = true;  // cost-model planner (false: greedy packing)
   bool kv = false; // key-value plan: 16 pairs per thread, 2^12 / 2^13 tiles
   int cmerge = 0;  // merge-pass coset size when it differs from the tile (0 = auto)
+  bool mixed_c = true;         // choose the coset size per merge pass (tile's or cmerge)
+  double wide_tail_cost = 0.2; // extra cost of a tail pass on the larger cosets
   double trip_cost = 0.10;  // extra cost of a shared-memory round trip, in passes
 };
 
@@ -218,7 +220,10 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // ALU-bound (smaller tiles do fewer steps per key), the merge passes are
   // HBM-bound (larger cosets need fewer passes).
   // Measured on B200 (13-bit tile + 14-bit merges vs 13/13): 2^26 2.50 vs
-  // 2.57 ms, 2^28 equal, 2^30 54.4 vs 56.6 ms; 2^24 prefers 13/13.
+  // 2.57 ms, 2^28 equal, 2^30 54.4 vs 56.6 ms; 2^24 prefers 13/13.  With the
+  // coset size chosen per pass (mixed_c: 14-bit middle passes, 13-bit tail
+  // passes where the wide ones are register-limited): 2^26 2.42, 2^28 10.97,
+  // 2^30 52.9 ms.
   const int CT = C;
   int cm = opt.cmerge;
   if (cm == 0 && opt.cmin != opt.cmax && k >= 26) cm = 14;
@@ -267,54 +272,73 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     // Dynamic program over (phase p, next step bit b): each pass costs 1 plus
     // trip_cost per extra shared-memory round trip; shapes are restricted to
     // the instantiated kernel families (tail-only, tail+head with a = b+1,
-    // middle runs of h high bits).
+    // middle runs of h high bits).  With opt.mixed_c every pass may instead
+    // use the tile's coset size (CT) or the merge coset size (C); the larger
+    // cosets' tail passes are charged opt.wide_tail_cost more (they run at 2
+    // CTAs per SM, measured on B200).
     const int K = k + 2;
     std::vector<double> best((size_t)K * K, -1.0);
     std::vector<int> choice((size_t)K * K, 0);  // 0 tail-only, >0 tail+head h, <0 middle -h
-    auto cost_of = [&](int SA, int SB) {
-      return 1.0 + opt.trip_cost * (detail::merge_trips(C, R, SA, SB) - 1);
+    std::vector<int> choice_c((size_t)K * K, C);
+    std::vector<int> cands = {C};
+    if (opt.mixed_c && CT < C && CT >= 12) cands = {C, CT};
+    auto cost_of = [&](int Cc, int SA, int SB) {
+      double c = 1.0 + opt.trip_cost * (detail::merge_trips(Cc, R, SA, SB) - 1);
+      if (Cc > CT && SA >= 0) c += opt.wide_tail_cost;
+      return c;
     };
     std::function<double(int, int)> solve = [&](int p, int b) -> double {
       if (p > k) return 0.0;
       double& memo = best[(size_t)p * K + b];
       if (memo >= 0) return memo;
       double bc = 1e30;
-      int bch = 0;
-      if (b < C) {
-        // A tail-only pass takes phase p's direction as CTA-uniform: valid
-        // only when bit p lies above the coset (p >= C; after a smaller tile
-        // sort, p < C happens and the tail must be fused with a head).
-        if (p >= C) {
-          bc = cost_of(b, -1) + solve(p + 1, p);
-          bch = 0;
-        }
-        const int h = C - (b + 1);
-        // tail+head: phase p's direction bit must be the coset's top local
-        // bit C-1 (p >= C-1), which also keeps the head above the tail
-        if (p < k && p >= C - 1 && b + 1 >= lrun && h >= 1) {
-          const double t1 = cost_of(b, b + 1) + solve(p + 1, p - h);
-          if (t1 < bc) {
-            bc = t1;
-            bch = h;
+      int bch = 0, bcc = C;
+      for (int Cc : cands) {
+        if (b < Cc) {
+          // A tail-only pass takes phase p's direction as CTA-uniform: valid
+          // only when bit p lies above the coset (p >= Cc; after a smaller
+          // tile sort, p < Cc happens and the tail must be fused with a head).
+          if (p >= Cc) {
+            const double t0 = cost_of(Cc, b, -1) + solve(p + 1, p);
+            if (t0 < bc - 1e-9) {
+              bc = t0;
+              bch = 0;
+              bcc = Cc;
+            }
           }
-        }
-      } else {
-        for (int h = 1; h <= C - lrun && h <= b; ++h) {
-          const double t = cost_of(-1, C - h) + solve(p, b - h);
-          if (t < bc - 1e-9) {
-            bc = t;
-            bch = -h;
+          const int h = Cc - (b + 1);
+          // tail+head: phase p's direction bit must be the coset's top local
+          // bit Cc-1 (p >= Cc-1), which also keeps the head above the tail
+          if (p < k && p >= Cc - 1 && b + 1 >= lrun && h >= 1) {
+            const double t1 = cost_of(Cc, b, b + 1) + solve(p + 1, p - h);
+            if (t1 < bc - 1e-9) {
+              bc = t1;
+              bch = h;
+              bcc = Cc;
+            }
+          }
+        } else {
+          for (int h = 1; h <= Cc - lrun && h <= b; ++h) {
+            const double t = cost_of(Cc, -1, Cc - h) + solve(p, b - h);
+            if (t < bc - 1e-9) {
+              bc = t;
+              bch = -h;
+              bcc = Cc;
+            }
           }
         }
       }
       choice[(size_t)p * K + b] = bch;
+      choice_c[(size_t)p * K + b] = bcc;
       memo = bc;
       return bc;
     };
     solve(CT + 1, CT);
     int p = CT + 1, b = CT;
+    const int Cmax = C;
     while (p <= k) {
       const int ch = choice[(size_t)p * K + b];
+      C = choice_c[(size_t)p * K + b];  // the push helpers read C
       if (b < C) {
         push_tail_head(p, b, ch);
         if (ch > 0) {
@@ -329,6 +353,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
         b -= -ch;
       }
     }
+    C = Cmax;
     return plan;
   }
 

@@ -59,7 +59,8 @@ struct GraphKey {
   uint64_t n, batch;
   uint32_t kx;
   int cmax, cmin, lrun, regbits, tile_regbits, cmerge, dp, generic, pdl;
-  double trip_cost;
+  double trip_cost, wide_tail_cost;
+  int mixed_c;
   bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 struct GraphEntry {
