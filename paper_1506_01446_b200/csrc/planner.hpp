@@ -133,7 +133,7 @@ struct PlanOptions {
   bool kv = false; // key-value plan: 16 pairs per thread, 2^12 / 2^13 tiles
   int cmerge = 0;  // merge-pass coset size when it differs from the tile (0 = auto)
   bool mixed_c = true;         // choose the coset size per merge pass (tile's or cmerge)
-  double wide_tail_cost = 0.2; // extra cost of a tail pass on the larger cosets
+  double wide_tail_cost = -1;  // extra cost of a tail pass on the larger cosets (<0: auto)
   double trip_cost = 0.10;  // extra cost of a shared-memory round trip, in passes
 };
 
@@ -222,11 +222,11 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // Measured on B200 (13-bit tile + 14-bit merges vs 13/13): 2^26 2.50 vs
   // 2.57 ms, 2^28 equal, 2^30 54.4 vs 56.6 ms; 2^24 prefers 13/13.  With the
   // coset size chosen per pass (mixed_c: 14-bit middle passes, 13-bit tail
-  // passes where the wide ones are register-limited): 2^26 2.42, 2^28 10.97,
-  // 2^30 52.9 ms.
+  // passes where the wide ones are register-limited): 2^24 0.471 (vs 0.481),
+  // 2^25 1.157, 2^26 2.405, 2^28 10.97, 2^30 52.9 ms.
   const int CT = C;
   int cm = opt.cmerge;
-  if (cm == 0 && opt.cmin != opt.cmax && k >= 26) cm = 14;
+  if (cm == 0 && opt.cmin != opt.cmax && k >= 24) cm = 14;
   // (cm <= C + 2: the first merge state, phase C+1 from bit C, must have its
   // direction bit at or above local bit cm-1 -- see the tail-only / tail+head
   // rules in the DP below.)
@@ -282,9 +282,11 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     std::vector<int> choice_c((size_t)K * K, C);
     std::vector<int> cands = {C};
     if (opt.mixed_c && CT < C && CT >= 12) cands = {C, CT};
+    // measured best: 0.3 up to 2^26 keys, 0.2 above
+    const double wide_tail = opt.wide_tail_cost >= 0 ? opt.wide_tail_cost : (k <= 26 ? 0.3 : 0.2);
     auto cost_of = [&](int Cc, int SA, int SB) {
       double c = 1.0 + opt.trip_cost * (detail::merge_trips(Cc, R, SA, SB) - 1);
-      if (Cc > CT && SA >= 0) c += opt.wide_tail_cost;
+      if (Cc > CT && SA >= 0) c += wide_tail;
       return c;
     };
     std::function<double(int, int)> solve = [&](int p, int b) -> double {
