@@ -281,12 +281,13 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     std::vector<int> choice((size_t)K * K, 0);  // 0 tail-only, >0 tail+head h, <0 middle -h
     std::vector<int> choice_c((size_t)K * K, C);
     std::vector<int> cands = {C};
-    if (opt.mixed_c && CT < C && CT >= 12) cands = {C, CT};
+    if (opt.mixed_c && CT < C && CT >= 12)
+      for (int c = C - 1; c >= CT; --c) cands.push_back(c);
     // measured best: 0.3 up to 2^26 keys, 0.2 above
     const double wide_tail = opt.wide_tail_cost >= 0 ? opt.wide_tail_cost : (k <= 26 ? 0.3 : 0.2);
     auto cost_of = [&](int Cc, int SA, int SB) {
       double c = 1.0 + opt.trip_cost * (detail::merge_trips(Cc, R, SA, SB) - 1);
-      if (Cc > CT && SA >= 0) c += wide_tail;
+      if (Cc > CT && SA >= 0) c += wide_tail * (Cc - CT);
       return c;
     };
     std::function<double(int, int)> solve = [&](int p, int b) -> double {
