@@ -283,8 +283,9 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     std::vector<int> cands = {C};
     if (opt.mixed_c && CT < C && CT >= 12)
       for (int c = C - 1; c >= CT; --c) cands.push_back(c);
-    // measured best: 0.3 up to 2^26 keys, 0.2 above
-    const double wide_tail = opt.wide_tail_cost >= 0 ? opt.wide_tail_cost : (k <= 26 ? 0.3 : 0.2);
+    // measured best on B200: 0.3 up to 2^26 keys, 0.2 for 2^27..2^28, 0.1 above
+    const double wide_tail = opt.wide_tail_cost >= 0 ? opt.wide_tail_cost
+                             : (k <= 26 ? 0.3 : (k <= 28 ? 0.2 : 0.1));
     auto cost_of = [&](int Cc, int SA, int SB) {
       double c = 1.0 + opt.trip_cost * (detail::merge_trips(Cc, R, SA, SB) - 1);
       if (Cc > CT && SA >= 0) c += wide_tail * (Cc - CT);
