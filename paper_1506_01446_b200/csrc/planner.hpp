@@ -232,7 +232,9 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // rules in the DP below.)
   if (cm > C && cm <= C + 2 && cm <= 15 && cm <= kt && !opt.kv && batch == 1) {
     C = cm;
-    R = opt.regbits > 0 ? opt.regbits : 5;
+    // 16 keys per thread stays for the latency-bound sizes (16-key merge
+    // kernels exist for 2^12- and 2^13-key cosets); 32 elsewhere
+    R = opt.regbits > 0 ? opt.regbits : (R == 4 && C <= 13 ? 4 : 5);
   }
   const int lrun = opt.lrun;
   auto push_tail_head = [&](int p, int b, int h) {
