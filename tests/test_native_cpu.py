@@ -168,6 +168,27 @@ def test_emulated_plan_small_tiles(orc):
         b200.set_tuning(0, 5)
 
 
+@pytest.mark.parametrize("tile,merge,k", [(12, 13, 16), (12, 14, 16), (12, 14, 18),
+                                          (13, 14, 17), (13, 14, 18)])
+def test_emulated_mixed_coset_plans(orc, monkeypatch, tile, merge, k):
+    """Plans whose merge passes pick their coset size per pass (between the
+    tile's and the merge override; the default from 2^24 keys) must still
+    apply exactly the reference's step sequence: emulate them step by step
+    on the CPU."""
+    monkeypatch.setenv("B200_BITONIC_CMERGE", str(merge))
+    monkeypatch.setenv("B200_BITONIC_WIDE_TAIL_COST", "0.2")
+    b200.set_tuning(tile, 5)
+    try:
+        pl = b200.plan(1 << k)
+        sizes = {p.tile_bits for p in pl[1:]}
+        assert sizes <= set(range(tile, merge + 1)) and len(sizes) >= 2, sizes
+        x = orc.generate_input(1 << k, 500 + k)
+        assert (emulate_plan(x, k) == np.sort(x)).all(), (tile, merge, k)
+        assert (emulate_plan(x, k, descending=True) == np.sort(x)[::-1]).all()
+    finally:
+        b200.set_tuning(0, 5)
+
+
 def test_emulated_plan_batched(orc):
     x = orc.generate_input(8 * 1024, 3)
     out = emulate_plan(x, 10, batch=8)
