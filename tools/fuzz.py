@@ -1,5 +1,5 @@
 """Long randomized cross-check of every device entry point against numpy
-(development tool; run on a GPU box: python tools/fuzz.py SECONDS)."""
+(development tool; run on a GPU box: python tools/fuzz.py SECONDS [SEED [KMAX]])."""
 import os, sys, time
 import numpy as np
 import torch
@@ -9,6 +9,7 @@ import paper_1506_01446_b200 as b
 dev = torch.device("cuda:0")
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+kmax = int(sys.argv[3]) if len(sys.argv) > 3 else 23  # largest log2 length
 t0 = time.time()
 n_cases = 0
 fails = []
@@ -21,7 +22,7 @@ def tot64(u):
 while time.time() - t0 < budget:
     kind = rng.choice(["sort", "padded", "batched", "pairs", "f32", "i64", "f64", "planes"])
     desc = bool(rng.integers(0, 2))
-    k = int(rng.integers(1, 24))
+    k = int(rng.integers(1, kmax + 1))
     n = 1 << k
     try:
         if kind in ("sort", "padded", "batched", "pairs"):
