@@ -1,25 +1,36 @@
 #!/usr/bin/env python3
 """bench.py -- device-timed Gkeys/s of the B200 bitonic sort (BASELINE.json metric).
 
-Default (N=1): BASELINE.json configs[1], 2^20 random uint32 keys on one B200,
-ascending.  One "step" = one full sort of the 2^20-key array.  The unsorted
-input is restored (device-to-device copy) and L2 is flushed (a 256 MiB write,
-larger than the 126 MB L2) before every step, outside the timed region; each
-step is timed with CUDA events on the sorting stream and the K durations are
-summed.  Under torchrun (N>1) every rank owns a 2^20-key shard of one
-N*2^20-key array and the partitioned sort (local sort + NCCL merge-split
-network, paper_1506_01446_b200/dist.py) is timed, max over ranks ("weak").
+Default (N=1): BASELINE.json configs[2]'s 2^28 point -- the largest
+single-GPU configuration, north_star's primary HBM-bound size and the
+paper's largest Table-1 row: 2^28 keys from the reference's
+own ``generate_input(n, seed=1)`` (bench.cpp:354-364: low 32 bits of
+std::mt19937_64(1)), sorted ascending as uint32.  The GPU arm, its
+``cpu_baseline`` leg and ``--impl reference`` all sort that same buffer (the
+reference's CPU code sorts it as int32 after x ^ 0x80000000, the exact
+uint32-order bridge), and both arms print the same ``config`` dict.
+
+One "step" = one full in-place sort of the array.  The unsorted input is
+restored (device-to-device copy) and L2 is flushed (a 256 MiB write, larger
+than the 126 MB L2; the 1 GiB array is itself 8x L2) before every step,
+outside the timed region; each step is timed with CUDA events on the sorting
+stream.  Under torchrun (N>1) every rank owns a 2^(32 - log2 N)-key shard of
+one 2^32-key array (BASELINE configs[4]) and the partitioned sort (local sort
++ merge-split network, paper_1506_01446_b200/dist.py) is timed, max over
+ranks ("strong").  ``--log2n`` / ``--batched`` select the other configs.
 
 Extra JSON keys (see the task contract): e2e (host pinned buffers, H2D + sort
-+ D2H inside the timed region), roofline (dominant kernel family, measured
-live with CUDA events per launch), sort_roofline (north_star's whole-sort
-definition: P_min x 8 bytes x n / HBM BW), cpu_baseline (the reference's own
-CPU code from oracle/_ref, timed on this host), clocks (nvidia-smi sampled
++ D2H inside the timed region, through the reference-facing host entry),
+roofline (dominant kernel family, measured live with CUDA events), sort_roofline
+(north_star's whole-sort definition: P_min x 8 bytes x n / HBM BW),
+cpu_baseline (the reference's own CPU code from oracle/_ref on this host,
+with its output compared key for key with the GPU's), clocks (NVML sampled
 during the timed region), gpu_launches.
 
 ``--impl reference`` times the reference's CPU implementation of the path
-(oracle/_ref: bitonic::execute(build_plan(fused, 1024)) on all host threads)
-on the same workload and prints the same line with "impl": "reference".
+(oracle/_ref: generate_schedule + build_plan(fused, 1024) + execute on all
+host threads, run_cell's timing discipline, bench.cpp:68-116) on the same
+workload and prints the same line with "impl": "reference".
 """
 from __future__ import annotations
 
@@ -30,6 +41,7 @@ import subprocess
 import sys
 import threading
 import time
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -38,6 +50,7 @@ sys.path.insert(0, ROOT)
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 METRIC = "Gkeys/s sorting uint32 (device-timed) vs HBM roofline; speedup vs CPU quicksort"
+SEED = 1  # generate_input's default seed (bench.cpp:354, BenchConfig)
 # P_min(k, c=15): minimum HBM round trips of the network.
 PMIN = {16: 3, 20: 7, 24: 13, 28: 21, 29: 22, 30: 24, 31: 27, 32: 29}
 
@@ -63,6 +76,24 @@ def peaks():
         return float(d["hbm_gbs"]), "measured", d
     except Exception:
         return HBM_FALLBACK, "fallback", {}
+
+
+def host_info():
+    """CPU model and core count of this host (the GPU box's, when run there)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "usable_cpus": usable}
 
 
 class ClockSampler:
@@ -175,76 +206,114 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
+# the workload (identical in both arms)
+# ---------------------------------------------------------------------------
+def resolve_args(args):
+    """Fill in log2n / scaling from the config the flags select."""
+    world = dist_env()[0]
+    args.scaling = "weak"
+    if args.log2n is None:
+        if args.batched:
+            args.log2n = 24
+        elif world > 1:
+            args.log2n = 32 - (world.bit_length() - 1)
+            args.scaling = "strong"  # 2^32 keys in all, whatever N
+        else:
+            args.log2n = 28
+    return args
+
+
+def workload_config(args, world):
+    """The config dict both arms print (the driver compares them)."""
+    n = 1 << args.log2n
+    total = n * world
+    if args.batched:
+        return {"workload": (f"batched: {n // args.batched} arrays of {args.batched} keys, "
+                             f"each sorted independently, ascending uint32; keys = "
+                             f"generate_input({n}, seed={SEED}) (bench.cpp:354-364)"),
+                "keys_total": total, "n_per_array": args.batched,
+                "arrays": n // args.batched, "seed": SEED}
+    if world > 1:
+        return {"workload": (f"2^{total.bit_length() - 1} keys, one array partitioned over "
+                             f"{world} GPUs (2^{args.log2n} per rank; shard r = "
+                             f"generate_input(2^{args.log2n}, seed={SEED}+r), "
+                             f"bench.cpp:354-364), ascending uint32"),
+                "keys_total": total, "keys_per_gpu": n, "seed": SEED}
+    return {"workload": (f"2^{args.log2n} keys = generate_input(2^{args.log2n}, seed={SEED}) "
+                         f"(bench.cpp:354-364: low 32 bits of std::mt19937_64), one array, "
+                         f"ascending uint32"),
+            "keys_total": total, "keys_per_gpu": n, "seed": SEED}
+
+
+# ---------------------------------------------------------------------------
 # reference arm (CPU): the reference's own code from oracle/_ref
 # ---------------------------------------------------------------------------
 def reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
-        return 0
-    import numpy as np
+        return 0  # rank 0 alone runs and prints the reference arm
     import oracle
     ref = oracle.reference()
-    n_config = (1 << args.log2n) * world
-    cores = os.cpu_count() or 1
+    cfg = workload_config(args, world)
+    info = host_info()
+    cores = info["usable_cpus"]
     if args.batched:
-        return reference_arm_batched(args, ref, 1 << args.log2n, cores)
-    # bounded sample of the configuration (the reference's CPU sort of 2^32
-    # keys would take minutes per step); throughput is per key
-    n = min(n_config, 1 << 22)
-    if ref is not None:
+        return reference_arm_batched(args, ref, cfg, info)
+    n_cfg = cfg["keys_total"]
+    # N=1: the whole workload.  N>1: the 2^32-key workload would take ~2 min
+    # per step on the CPU; a 2^28-key sample of it (rank 0's generator
+    # stream) keeps the run within minutes.
+    n = n_cfg if world == 1 else min(n_cfg, 1 << 28)
+    if ref is not None and ref.has_bench:
         kind = "reference"
-        rng = np.random.default_rng(1)
-        x = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+        x = ref.generate_input(n, SEED)  # the reference's own generator (int32 bits)
+        x ^= np.int32(-2**31)            # u32 order == i32 order of x ^ 0x80000000
         work = x.copy()
-        run = lambda: ref.execute_inplace(work, 2, min(1024, n), cores)
-        what = f"bitonic::execute(build_plan(fused, {min(1024, n)}), keys, {cores} workers)"
-        if n < n_config:
-            what += f" on a 2^{n.bit_length() - 1}-key sample of the 2^{n_config.bit_length() - 1}-key workload"
+
+        def run():
+            return ref.execute_timed_inplace(work, 2, min(1024, n), cores) * 1e-3
+        what = (f"bitonic::execute(build_plan(generate_schedule({n.bit_length() - 1}), fused, "
+                f"{min(1024, n)}), keys, {cores} workers), timed as run_cell does "
+                f"(bench.cpp:92-107)")
+        if n < n_cfg:
+            what += (f", on a 2^{n.bit_length() - 1}-key sample of the "
+                     f"2^{n_cfg.bit_length() - 1}-key workload")
     else:  # pragma: no cover - oracle port when the reference was not built
         kind = "port"
         o = oracle.oracle()
-        x = o.generate_input(n, 1).view(np.int32)
+        x = (o.generate_input(n, SEED) ^ np.uint32(0x80000000)).view(np.int32)
         work = x.copy()
-        run = lambda: work.__setitem__(slice(None), o.sequential_bitonic_i32(work))
+
+        def run():
+            t0 = time.perf_counter()
+            work[:] = o.sequential_bitonic_i32(work)
+            return time.perf_counter() - t0
         what = "oracle sequential_bitonic_i32 (1 core)"
         cores = 1
-    for _ in range(args.warmup):
+    warm = args.warmup
+    for _ in range(warm):
         work[:] = x
         run()
     times = []
     for _ in range(args.steps):
         work[:] = x
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-    assert (np.diff(work.astype(np.int64)) >= 0).all()
+        times.append(run())
+    assert (np.diff(work.astype(np.int64)) >= 0).all(), "reference output not sorted"
     ms = 1e3 * sum(times) / len(times)
     value = n / (ms * 1e-3) / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gkeys/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": warm,
         "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": (f"2^{n_config.bit_length() - 1} random uint32 keys, ascending "
-                                f"(CPU{', sampled' if n < n_config else ''})"),
-                   "keys": n_config, "sample_keys": n},
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": cores,
-                         "kind": kind, "sample": what},
+                         "kind": kind, "sample": what, "sample_keys": n, **info},
         "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def _array_sample(n_per: int, total_arrays: int, target_keys: int = 1 << 22):
-    """A bounded sample of the batched workload: the first arrays of the same
-    generator stream, about target_keys keys in all."""
-    import numpy as np
-    count = max(1, min(total_arrays, target_keys // n_per))
-    rng = np.random.default_rng(1)
-    x = rng.integers(-2**31, 2**31, count * n_per, dtype=np.int64).astype(np.int32)
-    return x.reshape(count, n_per)
 
 
 def _per_array_parallel(fn, arrays, cores):
@@ -260,25 +329,27 @@ def _per_array_parallel(fn, arrays, cores):
         list(ex.map(fn, rows))
 
 
-def reference_arm_batched(args, ref, n, cores):
+def reference_arm_batched(args, ref, cfg, info):
     """Reference arm for the batched config: the reference's own
-    sequential_bitonic_sort on every array of a bounded sample of the
-    workload, arrays spread over all host cores (the reference has no batched
-    entry; one array per call is its API)."""
-    import numpy as np
+    sequential_bitonic_sort on every array of the workload, arrays spread
+    over all host cores (the reference has no batched entry; one array per
+    call is its API)."""
     n_per = args.batched
-    x = _array_sample(n_per, n // n_per)
-    work = x.copy()
-    if ref is not None:
+    n = cfg["keys_total"]
+    cores = info["usable_cpus"]
+    if ref is not None and ref.has_bench:
+        x = (ref.generate_input(n, SEED) ^ np.int32(-2**31)).reshape(-1, n_per)
         kind, fn = "reference", ref.sequential_bitonic_sort_inplace
-        what = (f"bitonic::sequential_bitonic_sort on {x.shape[0]} of the {n // n_per} "
-                f"arrays of {n_per} keys, {cores} threads")
+        what = (f"bitonic::sequential_bitonic_sort on each of the {x.shape[0]} arrays of "
+                f"{n_per} keys, {cores} threads")
     else:  # pragma: no cover
         import oracle
         o = oracle.oracle()
+        x = (o.generate_input(n, SEED) ^ np.uint32(0x80000000)).view(np.int32).reshape(-1, n_per)
         kind = "port"
         fn = lambda a: a.__setitem__(slice(None), o.sequential_bitonic_i32(a))
         what = f"oracle sequential_bitonic_i32 on {x.shape[0]} arrays, {cores} threads"
+    work = x.copy()
     for _ in range(args.warmup):
         work[:] = x
         _per_array_parallel(fn, work, cores)
@@ -295,13 +366,10 @@ def reference_arm_batched(args, ref, n, cores):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gkeys/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms * (n / work.size), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"batched: {n // n_per} arrays of {n_per} random uint32 "
-                               f"keys (CPU, sampled)", "keys": n,
-                   "sample_keys": int(work.size)},
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": cores,
-                         "kind": kind, "sample": what},
+                         "kind": kind, "sample": what, "sample_keys": int(work.size), **info},
         "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -309,77 +377,77 @@ def reference_arm_batched(args, ref, n, cores):
     return 0
 
 
-def cpu_baseline_batched(n_per: int, total_arrays: int, budget_s: float = 12.0):
-    """Batched workload on the host: the paper's quicksort per array (1 core)
-    and the reference's sequential bitonic per array over all cores, on a
-    bounded sample of the arrays."""
+# ---------------------------------------------------------------------------
+# cpu_baseline leg of our arm (rank 0, N=1): the same buffer on the host
+# ---------------------------------------------------------------------------
+def cpu_baseline(x_u32: np.ndarray, gpu_sorted_u32: np.ndarray, info):
+    """The paper's CPU quicksort (1 core, the paper's speedup baseline,
+    verify.cpp:109-116) and the reference's CPU bitonic sorts on the SAME keys
+    the GPU sorted; the reference fused engine's output is compared key for
+    key with the GPU's (run_cell's check, bench.cpp:68-116)."""
     import oracle
     ref = oracle.reference()
-    x = _array_sample(n_per, total_arrays)
-    cores = os.cpu_count() or 1
-    if ref is None:
+    n = x_u32.size
+    x = (x_u32 ^ np.uint32(0x80000000)).view(np.int32)  # int32 order == u32 order of x
+    cores = info["usable_cpus"]
+    out = {}
+    if ref is None:  # pragma: no cover
+        o = oracle.oracle()
+        kind = "port"
+        t0 = time.perf_counter()
+        qs = o.quicksort_i32(x)
+        out["quicksort_ms"] = (time.perf_counter() - t0) * 1e3
+        ref_sorted = qs
+    else:
+        kind = "reference"
+        w = x.copy()
+        t0 = time.perf_counter()
+        ref.quicksort_inplace(w)  # one rep: ~25 s at 2^28 on one core
+        out["quicksort_ms"] = (time.perf_counter() - t0) * 1e3
+        w = x.copy()
+        out["fused_engine_ms"] = ref.execute_timed_inplace(w, 2, min(1024, n), cores)
+        out["fused_engine_cores"] = cores
+        ref_sorted = w
+        # sequential bitonic (1 core) costs ~2 min at 2^28: time it on the
+        # first 2^min(k,24) keys and say so
+        ns = min(n, 1 << 24)
+        w = x[:ns].copy()
+        t0 = time.perf_counter()
+        ref.sequential_bitonic_sort_inplace(w)
+        out["sequential_bitonic_ms"] = (time.perf_counter() - t0) * 1e3
+        out["sequential_bitonic_keys"] = ns
+    got = gpu_sorted_u32 ^ np.uint32(0x80000000)
+    out["gpu_output_equals_reference"] = bool(np.array_equal(got.view(np.int32), ref_sorted))
+    return kind, cores, out
+
+
+def cpu_baseline_batched(x_u32: np.ndarray, n_per: int, info):
+    """Batched workload on the host: the paper's quicksort per array (1 core)
+    on a bounded sample of the arrays, and the reference's sequential bitonic
+    on every array over all cores."""
+    import oracle
+    ref = oracle.reference()
+    arrays = (x_u32 ^ np.uint32(0x80000000)).view(np.int32).reshape(-1, n_per)
+    cores = info["usable_cpus"]
+    sample = arrays[: max(1, min(arrays.shape[0], (1 << 22) // n_per))]
+    if ref is None:  # pragma: no cover
         o = oracle.oracle()
         kind = "port"
         qs = lambda a: a.__setitem__(slice(None), o.quicksort_i32(a))
         seq = lambda a: a.__setitem__(slice(None), o.sequential_bitonic_i32(a))
     else:
         kind, qs, seq = "reference", ref.quicksort_inplace, ref.sequential_bitonic_sort_inplace
-    t_start = time.perf_counter()
-
-    def best(fn, c, reps):
-        b = float("inf")
-        for _ in range(reps):
-            w = x.copy()
-            t0 = time.perf_counter()
-            _per_array_parallel(fn, w, c)
-            b = min(b, time.perf_counter() - t0)
-            if time.perf_counter() - t_start > budget_s:
-                break
-        return b
-    out = {"sample_arrays": int(x.shape[0]), "sample_keys": int(x.size)}
-    out["quicksort_ms"] = 1e3 * best(qs, 1, 3)
-    out["sequential_bitonic_all_cores_ms"] = 1e3 * best(seq, cores, 3)
-    return kind, cores, out
-
-
-def cpu_baseline(n: int, budget_s: float = 12.0):
-    """The paper's CPU quicksort and the reference's CPU bitonic sorts, timed
-    on this host on the same workload (oracle/_ref = the reference's code)."""
-    import numpy as np
-    import oracle
-    ref = oracle.reference()
-    rng = np.random.default_rng(1)
-    x = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
-    cores = os.cpu_count() or 1
-    out = {}
-    if ref is None:
-        o = oracle.oracle()
-        kind, qs = "port", (lambda a: a.__setitem__(slice(None), o.quicksort_i32(a)))
-        seq = lambda a: a.__setitem__(slice(None), o.sequential_bitonic_i32(a))
-        fused = None
-    else:
-        kind = "reference"
-        qs = ref.quicksort_inplace
-        seq = ref.sequential_bitonic_sort_inplace
-        fused = lambda a: ref.execute_inplace(a, 2, min(1024, n), cores)
-    t_start = time.perf_counter()
-
-    def best(fn, reps):
-        b = float("inf")
-        for _ in range(reps):
-            w = x.copy()
-            t0 = time.perf_counter()
-            fn(w)
-            b = min(b, time.perf_counter() - t0)
-            if time.perf_counter() - t_start > budget_s:
-                break
-        return b
-
-    out["quicksort_ms"] = 1e3 * best(qs, 5)
-    out["sequential_bitonic_ms"] = 1e3 * best(seq, 3)
-    if fused is not None:
-        out["fused_engine_ms"] = 1e3 * best(fused, 3)
-    return kind, cores, out
+    out = {"sample_arrays": int(sample.shape[0]), "sample_keys": int(sample.size)}
+    w = sample.copy()
+    t0 = time.perf_counter()
+    _per_array_parallel(qs, w, 1)
+    out["quicksort_ms"] = (time.perf_counter() - t0) * 1e3
+    w = arrays.copy()
+    t0 = time.perf_counter()
+    _per_array_parallel(seq, w, cores)
+    out["sequential_bitonic_all_cores_ms"] = (time.perf_counter() - t0) * 1e3
+    out["all_keys"] = int(arrays.size)
+    return kind, cores, out, w
 
 
 # ---------------------------------------------------------------------------
@@ -392,29 +460,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--log2n", type=int, default=None,
-                    help="keys per GPU = 2^log2n.  Default: 20 at N=1 (BASELINE "
-                         "configs[1]); 32 - log2(N) at N>1 (configs[4]: 2^32 keys "
-                         "partitioned over the N GPUs); 24 with --batched (configs[3])")
+                    help="keys per GPU = 2^log2n.  Default: 28 at N=1 (BASELINE "
+                         "configs[2], the largest single-GPU config); 32 - log2(N) at N>1 "
+                         "(configs[4]: 2^32 keys partitioned over the N GPUs); 24 with "
+                         "--batched (configs[3])")
     ap.add_argument("--batched", type=int, default=0,
                     help="n_per_array for the batched config (e.g. 4096)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    args.scaling = "weak"
-    if args.log2n is None:
-        world0 = dist_env()[0]
-        if args.batched:
-            args.log2n = 24
-        elif world0 > 1:
-            args.log2n = 32 - (world0.bit_length() - 1)
-            args.scaling = "strong"  # 2^32 keys in all, whatever N
-        else:
-            args.log2n = 20
+    resolve_args(args)
 
     if args.impl == "reference":
         return reference_arm(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_1506_01446_b200 as b200
@@ -425,7 +484,7 @@ def main():
     # Functional test hook (never a measurement): B200_BENCH_SHARED_GPU=1 runs
     # every rank on cuda:0 with gloo, to exercise the N>1 code path on a
     # one-GPU box.  The ranks' kernels never wait on each other (the peer
-    # exchange is ordered by host barriers).
+    # exchange is ordered by host-side events).
     shared_gpu = world > 1 and os.environ.get("B200_BENCH_SHARED_GPU") == "1"
     if shared_gpu:
         local = 0
@@ -438,21 +497,23 @@ def main():
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
+    info = host_info()
+    cfg = workload_config(args, world)
 
     n = 1 << args.log2n
     hbm, peak_kind, peaks_json = peaks()
-    g = torch.Generator(device=dev)
-    g.manual_seed(1 + rank)
-    src = torch.randint(-2**31, 2**31, (n,), dtype=torch.int64, device=dev,
-                        generator=g).to(torch.int32).view(torch.uint32)
+    # the reference's generate_input bits (product host function, same
+    # algorithm as bench.cpp:354-364), generated outside any timing
+    x_host = b200.generate_input(n, SEED + (rank if world > 1 else 0))
+    src = torch.from_numpy(x_host.view(np.int32)).to(dev).view(torch.uint32)
     work = src.clone()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     batched = args.batched
+    dist_stats = {}
     if world > 1:
         from paper_1506_01446_b200 import dist as bdist
         exchange = os.environ.get("B200_BITONIC_EXCHANGE", "peer")
-        dist_stats = {}
 
         def sort_step():
             bdist.partitioned_sort_(work, exchange=exchange, stats=dist_stats)
@@ -460,23 +521,16 @@ def main():
         # local sort + one fused merge-split (partition + merge kernels) per
         # network step (the two shard copies are memcpys, not kernels)
         launches_per_step = len(plan) + 2 * len(bdist.network_steps(world))
-        workload = (f"{world}x2^{args.log2n} random uint32 keys, one array partitioned "
-                    f"over {world} GPUs (local sort + bitonic merge-split network; "
-                    f"exchange={exchange}: "
-                    + ("partner shard read over CUDA IPC peer memory inside the merge "
-                       "kernel" if exchange == "peer" else "NCCL send/recv") + ")")
     elif batched:
         def sort_step():
             b200.sort_batched_(work, batched)
         plan = b200.plan(batched, n // batched)
         launches_per_step = len(plan)
-        workload = f"batched: {n // batched} arrays of {batched} random uint32 keys"
     else:
         def sort_step():
             b200.sort_(work)
         plan = b200.plan(n)
         launches_per_step = len(plan)
-        workload = f"2^{args.log2n} random uint32 keys, one array, ascending"
 
     def barrier():
         if world > 1:
@@ -496,9 +550,13 @@ def main():
         else:
             ref = torch.sort(ref).values
         got = work.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-        if not torch.equal(got, ref):
+        ok = torch.equal(got, ref)
+        del ref, got
+        torch.cuda.empty_cache()
+        if not ok:
             print(json.dumps({"error": "sort output mismatch"}), flush=True)
             return 1
+    gpu_sorted = work.view(torch.int32).cpu().numpy().view(np.uint32) if world == 1 else None
 
     # ---- timed region ----------------------------------------------------------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -542,7 +600,7 @@ def main():
         # passes on the sort stream; pass i lasts e[i+1] - e[i].  (The events
         # break the programmatic-dependent-launch overlap, so these durations
         # are slightly longer than inside the graph-launched sort.)
-        fam_t, fam_n, fam_bytes = {}, {}, {}
+        fam_t, fam_n = {}, {}
         reps = 10
         for _ in range(reps):
             work.copy_(src)
@@ -570,13 +628,16 @@ def main():
         alg_bytes = 8 * n  # one read + one write of every key per launch
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
         traffic = None
-        try:  # measured DRAM bytes per launch from the committed ncu capture
-            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-                tr = json.load(f)
-            key = f"batched{batched}" if batched else str(args.log2n)
-            traffic = tr.get(key, {}).get(dom)
-        except Exception:
-            pass
+        for fname in ("traffic.json", "r1_traffic.json"):
+            try:  # measured DRAM bytes per launch from the committed ncu capture
+                with open(os.path.join(ROOT, "profiles", fname)) as f:
+                    tr = json.load(f)
+                key = f"batched{batched}" if batched else str(args.log2n)
+                traffic = tr.get(key, {}).get(dom)
+                if traffic is not None:
+                    break
+            except Exception:
+                pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                     "traffic": traffic,
@@ -605,12 +666,12 @@ def main():
     # device entry between explicit pinned copies, CUDA-event timed.
     e2e = None
     if world == 1:
-        h_src = src.cpu().pin_memory()
+        h_src = torch.from_numpy(x_host.view(np.int32)).pin_memory()
         h_out = torch.empty_like(h_src).pin_memory()
         dwork = torch.empty_like(src)
         tt = []
-        h_src_np = h_src.view(torch.int32).numpy()
-        arr = h_out.view(torch.int32).numpy().view(np.uint32)
+        h_src_np = h_src.numpy()
+        arr = h_out.numpy().view(np.uint32)
         for i in range(args.warmup + args.steps):
             flush.zero_()
             if not batched:
@@ -625,24 +686,23 @@ def main():
             else:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                dwork.copy_(h_src, non_blocking=True)
+                dwork.copy_(h_src.view(torch.uint32), non_blocking=True)
                 b200.sort_batched_(dwork, batched)
-                h_out.copy_(dwork, non_blocking=True)
+                h_out.view(torch.uint32).copy_(dwork, non_blocking=True)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 t_ms = e0.elapsed_time(e1)
             if i >= args.warmup:
                 tt.append(t_ms)
-        if not batched:
-            ok = bool(np.all(arr[1:] >= arr[:-1]))
-            if not ok:
-                raise SystemExit("e2e host sort produced unsorted output")
+        if not np.array_equal(arr, gpu_sorted):
+            raise SystemExit("e2e output differs from the device-entry output")
         ems = sum(tt) / len(tt)
         e2e = {"value": n / (ems * 1e-3) / 1e9, "unit": "Gkeys/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                "ms_per_step": ems, "host_buffers": "pinned",
                "api": ("b200_bitonic_sort_host_u32 (host clock)" if not batched
                        else "H2D + b200_bitonic_sort_u32_batched + D2H (CUDA events)")}
+        del dwork, h_src, h_out
 
     if world > 1:
         # Each rank: H2D of its shard from pinned host memory, the partitioned
@@ -650,7 +710,7 @@ def main():
         # steps (restoring GiB-sized pinned buffers on the host is slow).
         err = None
         try:
-            h_src = src.cpu().pin_memory()
+            h_src = torch.from_numpy(x_host.view(np.int32)).pin_memory()
             h_work = torch.empty_like(h_src).pin_memory()
         except Exception as ex:  # pragma: no cover
             err = repr(ex)[:200]
@@ -664,9 +724,9 @@ def main():
                 torch.cuda.synchronize()
                 barrier()
                 c0 = time.perf_counter()
-                work.copy_(h_work, non_blocking=True)
+                work.view(torch.int32).copy_(h_work, non_blocking=True)
                 sort_step()
-                h_work.copy_(work, non_blocking=True)
+                h_work.copy_(work.view(torch.int32), non_blocking=True)
                 torch.cuda.synchronize()
                 t_ms = (time.perf_counter() - c0) * 1e3
                 t = torch.tensor([t_ms], device=dev, dtype=torch.float64)
@@ -684,38 +744,45 @@ def main():
                    "d2h_bytes_per_step": 4 * keys_total,
                    "error": err or "pinned host buffers unavailable on some rank"}
 
-    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
+    # ---- CPU baseline (rank 0, N=1 only), on the same buffer -----------------
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline and batched:
         try:
-            kind, cores, c = cpu_baseline_batched(batched, n // batched)
+            kind, cores, c, ref_sorted = cpu_baseline_batched(x_host, batched, info)
             qs_gk = c["sample_keys"] / (c["quicksort_ms"] * 1e-3) / 1e9
+            same = bool(np.array_equal((gpu_sorted ^ np.uint32(0x80000000)).view(np.int32),
+                                       ref_sorted.reshape(-1)))
             cpu = {"value": qs_gk, "unit": "Gkeys/s", "cores": 1, "kind": kind,
                    "sample": f"bitonic::reference_quicksort on each of the first "
                              f"{c['sample_arrays']} of the {n // batched} arrays of "
-                             f"{batched} keys (1 core), min of reps",
+                             f"{batched} keys (1 core)",
                    "quicksort_ms": c["quicksort_ms"],
                    "sequential_bitonic_all_cores_ms": c["sequential_bitonic_all_cores_ms"],
-                   "sequential_bitonic_all_cores_gkeys": c["sample_keys"] / (
+                   "sequential_bitonic_all_cores_gkeys": c["all_keys"] / (
                        c["sequential_bitonic_all_cores_ms"] * 1e-3) / 1e9,
-                   "all_cores": cores,
-                   "speedup_vs_quicksort": value / qs_gk}
+                   "all_cores": cores, "gpu_output_equals_reference": same,
+                   "speedup_vs_quicksort": value / qs_gk, **info}
         except Exception as e:  # pragma: no cover - report, do not fail the bench
             cpu = {"value": None, "unit": "Gkeys/s", "cores": 0, "kind": "unavailable",
                    "sample": f"cpu baseline failed: {e}"}
     if world == 1 and rank == 0 and not args.no_cpu_baseline and not batched:
         try:
-            kind, cores, c = cpu_baseline(n)
+            kind, cores, c = cpu_baseline(x_host, gpu_sorted, info)
             qs_gk = n / (c["quicksort_ms"] * 1e-3) / 1e9
             cpu = {"value": qs_gk, "unit": "Gkeys/s", "cores": 1, "kind": kind,
-                   "sample": f"bitonic::reference_quicksort (the paper's CPU baseline, "
-                             f"verify.cpp:109) on the same 2^{args.log2n} keys, min of reps",
+                   "sample": (f"bitonic::reference_quicksort (the paper's CPU baseline, "
+                              f"verify.cpp:109-116) on the same 2^{args.log2n} keys, one rep, "
+                              f"1 core"),
                    "quicksort_ms": c["quicksort_ms"],
-                   "sequential_bitonic_ms": c["sequential_bitonic_ms"],
                    "fused_engine_ms": c.get("fused_engine_ms"),
-                   "fused_engine_cores": cores,
+                   "fused_engine_cores": c.get("fused_engine_cores"),
+                   "sequential_bitonic_ms": c.get("sequential_bitonic_ms"),
+                   "sequential_bitonic_keys": c.get("sequential_bitonic_keys"),
+                   "gpu_output_equals_reference": c["gpu_output_equals_reference"],
                    "speedup_vs_quicksort": c["quicksort_ms"] / ms,
-                   "speedup_vs_sequential_bitonic": c["sequential_bitonic_ms"] / ms}
+                   **info}
+            if c.get("fused_engine_ms"):
+                cpu["speedup_vs_fused_engine"] = c["fused_engine_ms"] / ms
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "error": str(e)}
 
@@ -724,15 +791,15 @@ def main():
             "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "u32", "data": "synthetic",
-            "config": {"workload": workload, "keys_per_gpu": n, "keys_total": keys_total,
-                       "l2_flush": "256 MiB write before every step (outside timing)",
+            "dtype": "u32", "data": "synthetic", "config": cfg,
+            "timing": {"l2_flush": "256 MiB write before every step (outside timing)",
                        "input_restore": "D2D copy before every step (outside timing)",
-                       "timing": "CUDA events on the sort stream around each step; a device "
+                       "events": "CUDA events on the sort stream around each step; a device "
                                  "sleep before the start event keeps host launch overhead out",
                        "passes": len(plan),
                        **({"exchange": ("half (peer unavailable)"
-                                        if dist_stats.get("peer_fallback") else exchange)}
+                                        if dist_stats.get("peer_fallback") else exchange),
+                           **{k: v for k, v in dist_stats.items() if k != "peer_fallback"}}
                           if world > 1 else {})},
             "e2e": e2e, "roofline": roofline, "sort_roofline": sort_roof,
             "cpu_baseline": cpu, "clocks": sampler.summary(),

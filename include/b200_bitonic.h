@@ -20,8 +20,12 @@
  * There is no CPU fallback: a missing/unsupported GPU is B200_CUDA_ERROR.
  *
  * Device-pointer entry points are stream-ordered and asynchronous: they
- * enqueue kernels on `stream` and return; they allocate nothing (bitonic is
- * in place).  They are reentrant per stream.
+ * enqueue kernels on `stream` and return.  The power-of-two 32-bit sorts
+ * (u32/i32/f32, batched, pairs) and u64_planes are in place and allocate
+ * nothing; the interleaved 64-bit entries, the padded entries (non-power-
+ * of-two lengths) and merge / merge_split take scratch from a retained
+ * per-device pool (b200_bitonic_release_scratch returns it).  They are
+ * reentrant per stream.
  */
 #ifndef B200_BITONIC_H
 #define B200_BITONIC_H
@@ -133,7 +137,9 @@ int b200_bitonic_sort_padded_i32(int32_t* d_keys, uint64_t n, int descending,
 
 /* Host-memory convenience entries: H2D copy, sort, D2H copy, synchronous.
  * Mirror sequential_bitonic_sort(std::span<int32_t>) exactly (in place on
- * caller-owned host memory).  These allocate device memory per call. */
+ * caller-owned host memory).  Device buffers: one block of 8 bytes per key
+ * per device, grown on demand and kept for later calls (after a 2^30-key
+ * sort that is 8 GiB); b200_bitonic_release_scratch frees it. */
 int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending);
 int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending);
 
@@ -187,6 +193,12 @@ int b200_bitonic_ipc_close(void* d_ptr);
 /* Stream-ordered device-to-device copy (moves a shard into / out of the
  * IPC buffers). */
 int b200_bitonic_copy(void* dst, const void* src, uint64_t bytes, b200_stream_t stream);
+
+/* The reference's benchmark input, generate_input(size, seed)
+ * (proj/src/bench.cpp:354-364): key i = the low 32 bits of the i-th output
+ * of std::mt19937_64(seed), written to host memory h_out[0..n).  Host only
+ * (no GPU needed); n >= 1 else B200_INVALID_SIZE. */
+int b200_bitonic_generate_input(uint32_t* h_out, uint64_t n, uint64_t seed);
 
 /* ---- plan introspection (host only, no GPU needed) ----------------------
  * One entry per kernel launch of the sort of `batch` arrays of n keys. */

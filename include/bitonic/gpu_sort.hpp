@@ -112,21 +112,46 @@ inline Counters counters(std::uint64_t n, std::uint64_t batch = 1) {
 }
 
 // Drop-in for bitonic::execute(const LaunchPlan&, KeyArray, unsigned)
-// (engine.hpp:86-92): takes the keys by value, returns them sorted with the
-// counters.  Any plan type with the reference's `k` member is accepted (its
-// strategy and block capacity describe CPU launches and are not used: the
-// GPU runs its own plan).  Same failures: keys.size() != 2^k throws
-// invalid_size_error, workers < 1 throws config_error.
+// (engine.hpp:86-92, engine.cpp:175-227): takes the keys by value, returns
+// them sorted with counters.  Any plan type with the reference's `k` member
+// is accepted; the GPU runs its own plan (the caller's strategy and block
+// capacity describe CPU launches).  Same failures in the same order as
+// engine.cpp:177-185: workers < 1 throws config_error first, then
+// keys.size() != 2^k throws invalid_size_error.
+//
+// Counters: when the plan carries the reference's `launches` list, r.counters
+// are that plan's, charged exactly as account() (engine.cpp:147-173) does --
+// one launch = n reads + n writes, (n/2) x steps compare-exchanges -- so
+// `r.counters == plan_totals(plan)` style assertions keep holding after the
+// swap.  For a plan type without `launches` they are the GPU plan's
+// (bitonic::gpu::counters(n)), in the same cost model.
+template <class Plan>
+inline Counters plan_counters(const Plan& plan, std::uint64_t n) {
+  if constexpr (requires { plan.launches.begin(); }) {
+    Counters c;
+    for (const auto& launch : plan.launches) {
+      c.kernel_launches += 1;
+      c.global_reads += n;
+      c.global_writes += n;
+      c.compare_exchanges += (n / 2) * static_cast<std::uint64_t>(launch.steps.size());
+    }
+    return c;
+  } else {
+    return counters(n);
+  }
+}
+
 template <class Plan>
 inline ExecutionResult execute(const Plan& plan, std::vector<std::int32_t> keys,
                                unsigned workers) {
+  if (workers < 1) throw config_error("execute: workers must be >= 1");
   if (plan.k >= 64 || keys.size() != (std::uint64_t{1} << plan.k)) {
     throw invalid_size_error("execute: key count does not match the plan's 2^k");
   }
-  if (workers < 1) throw config_error("execute: workers must be >= 1");
   sort(std::span<std::int32_t>(keys), true);
   const std::uint64_t n = keys.size();
-  return ExecutionResult{std::move(keys), counters(n)};
+  Counters c = plan_counters(plan, n);
+  return ExecutionResult{std::move(keys), c};
 }
 
 }  // namespace bitonic::gpu

@@ -176,6 +176,9 @@ class Reference:
         lib.ref_quicksort_i32.argtypes = [_i32p, ctypes.c_uint64]
         lib.ref_execute_i32.argtypes = [_i32p, ctypes.c_uint64, ctypes.c_int,
                                         ctypes.c_uint64, ctypes.c_uint, _u64p]
+        lib.ref_execute_timed_i32.argtypes = [_i32p, ctypes.c_uint64, ctypes.c_int,
+                                              ctypes.c_uint64, ctypes.c_uint,
+                                              ctypes.POINTER(ctypes.c_double)]
         lib.ref_plan_counters.argtypes = [ctypes.c_uint, ctypes.c_int,
                                           ctypes.c_uint64, _u64p]
         lib.ref_predicted_counts.argtypes = [ctypes.c_uint, _u64p, _u64p]
@@ -223,6 +226,17 @@ class Reference:
                                       workers, None)
         if rc:
             raise ValueError(f"reference error {rc}")
+
+    def execute_timed_inplace(self, a: np.ndarray, strategy: int = 2, cap: int = 1024,
+                              workers: int = 1) -> float:
+        """execute() in place, timed like run_cell (bench.cpp:92-107): plan
+        build + execute on the clock, the vector copies off it.  Returns ms."""
+        ms = ctypes.c_double(0.0)
+        rc = self.lib.ref_execute_timed_i32(_ptr(a, _i32p), a.size, strategy, cap,
+                                            workers, ctypes.byref(ms))
+        if rc:
+            raise ValueError(f"reference error {rc}")
+        return ms.value
 
     def plan_counters(self, k: int, strategy: int, cap: int):
         cnt = np.zeros(4, dtype=np.uint64)

@@ -21,6 +21,7 @@
 // Status codes follow the product's C ABI: 0 ok, 1 invalid_size_error,
 // 2 config_error, 5 other exception.  Nothing here is on the product path.
 #include <cstdint>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <span>
@@ -87,6 +88,29 @@ int ref_execute_i32(int32_t* keys, uint64_t n, int strategy, uint64_t cap,
       counters[2] = result.counters.global_writes;
       counters[3] = result.counters.compare_exchanges;
     }
+  });
+}
+
+// run_cell's timing discipline (bench.cpp:92-107): the keys are copied into
+// the vector outside the timed region; generate_schedule + build_plan +
+// execute are timed with steady_clock; *ms receives the elapsed time.
+int ref_execute_timed_i32(int32_t* keys, uint64_t n, int strategy, uint64_t cap,
+                          unsigned workers, double* ms) {
+  return guarded([&] {
+    if (n < 2 || (n & (n - 1)) != 0) {
+      throw bitonic::invalid_size_error("length must be a power of two");
+    }
+    unsigned k = 0;
+    while ((uint64_t{1} << k) < n) ++k;
+    bitonic::KeyArray v(keys, keys + n);
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto plan = bitonic::build_plan(
+        bitonic::generate_schedule(k), static_cast<bitonic::Strategy>(strategy),
+        cap);
+    auto result = bitonic::execute(plan, std::move(v), workers);
+    const auto t1 = std::chrono::steady_clock::now();
+    *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    std::memcpy(keys, result.keys.data(), n * sizeof(int32_t));
   });
 }
 

@@ -36,7 +36,7 @@ __all__ = [
     "InvalidSizeError", "ConfigError", "CudaError",
     "sort_", "sort_pairs_", "sort_planes_", "argsort", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
     "merge_split_", "merge_", "sort_multi", "plan", "counters", "set_tuning",
-    "PassPlan", "version", "library_path", "release_scratch",
+    "PassPlan", "version", "library_path", "release_scratch", "generate_input",
 ]
 
 
@@ -222,10 +222,22 @@ def sort_batched_(t, n_per_array: int, descending: bool = False, stream=None):
     return t
 
 
+def generate_input(n: int, seed: int = 1) -> np.ndarray:
+    """The reference's benchmark keys, generate_input(size, seed)
+    (bench.cpp:354-364): the low 32 bits of std::mt19937_64(seed), as a host
+    uint32 array (the reference stores the same bits as int32)."""
+    out = np.empty(int(n), dtype=np.uint32)
+    _check(_native.lib().b200_bitonic_generate_input(
+        ctypes.c_void_p(out.ctypes.data), int(n), int(seed)))
+    return out
+
+
 def sort_host(keys: np.ndarray, descending: bool = False) -> np.ndarray:
     """In-place sort of a host numpy int32/uint32 array (H2D, sort, D2H)."""
     if not isinstance(keys, np.ndarray) or not keys.flags["C_CONTIGUOUS"]:
         raise ConfigError("keys must be a C-contiguous numpy array")
+    if not keys.flags["WRITEABLE"]:
+        raise ConfigError("keys must be writeable (the sort is in place)")
     if keys.dtype == np.int32:
         fn = _native.lib().b200_bitonic_sort_host_i32
     elif keys.dtype == np.uint32:

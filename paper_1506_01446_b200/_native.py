@@ -37,6 +37,7 @@ EXPORTED = (
     "b200_bitonic_sort_padded_i32",
     "b200_bitonic_sort_host_i32",
     "b200_bitonic_sort_host_u32",
+    "b200_bitonic_generate_input",
     "b200_bitonic_sort_u32_multi",
     "b200_bitonic_merge_split_u32",
     "b200_bitonic_merge_u32",
@@ -104,6 +105,7 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_sort_padded_i32.argtypes = [vp, u64, i, vp]
     L.b200_bitonic_sort_host_i32.argtypes = [vp, u64, i]
     L.b200_bitonic_sort_host_u32.argtypes = [vp, u64, i]
+    L.b200_bitonic_generate_input.argtypes = [vp, u64, u64]
     L.b200_bitonic_sort_u32_multi.argtypes = [ctypes.POINTER(vp),
                                               ctypes.POINTER(ctypes.c_int), i, u64, i]
     L.b200_bitonic_merge_split_u32.argtypes = [vp, vp, u64, i, ctypes.c_uint32, vp, vp]

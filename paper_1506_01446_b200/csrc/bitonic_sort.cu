@@ -293,11 +293,19 @@ GraphKey make_key(int kind, const void* p0, const void* p1, uint64_t n, uint64_t
   return key;
 }
 
+GraphExecPtr own_exec(cudaGraphExec_t e) {
+  return GraphExecPtr(e, [](cudaGraphExec_t x) {
+    if (x) cudaGraphExecDestroy(x);
+  });
+}
+
 void drop_graphs() {
-  std::lock_guard<std::mutex> lk(g_graph_mu);
-  for (auto& e : g_graphs)
-    if (e.exec) cudaGraphExecDestroy(e.exec);
-  g_graphs.clear();
+  std::vector<GraphEntry> old;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    old.swap(g_graphs);
+  }
+  // execs still held by a launcher are destroyed when it lets go
 }
 
 // Validates and runs the whole plan (or only pass `only`, when >= 0).

@@ -5,6 +5,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <random>
 
 #include "runtime.hpp"
 
@@ -70,7 +71,9 @@ cudaError_t pipe_buffers(HostPipe& P, uint64_t n, uint64_t cor_words) {
   const size_t need = n * 8 + cor_words * 8;
   if (P.cap >= need) return cudaSuccess;
   if (P.block) {
-    cudaError_t e = cudaDeviceSynchronize();
+    // every earlier call on this pipe joined into comp[0] and was waited for
+    // (the caller holds P.mu); sync it anyway instead of the whole device
+    cudaError_t e = cudaStreamSynchronize(P.comp[0]);
     if (e != cudaSuccess) return e;
     drop_graphs();  // captured pipelines refer to the old block
     cudaFree(P.block);
@@ -232,6 +235,18 @@ int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending) {
 
 int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending) {
   return host_sort(h_keys, n, descending, 0u);
+}
+
+// The reference's bench input (generate_input, bench.cpp:354-364): the low
+// 32 bits of successive std::mt19937_64(seed) outputs.  Host-side input
+// generation for benchmarks and callers that want the reference's workload;
+// not part of the sort.
+int b200_bitonic_generate_input(uint32_t* h_out, uint64_t n, uint64_t seed) {
+  if (n < 1) return fail(B200_INVALID_SIZE, "input size must be >= 1");
+  if (h_out == nullptr) return fail(B200_CONFIG, "null output pointer");
+  std::mt19937_64 rng(seed);
+  for (uint64_t i = 0; i < n; ++i) h_out[i] = static_cast<uint32_t>(rng());
+  return B200_OK;
 }
 
 }  // extern "C"

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -63,10 +64,15 @@ struct GraphKey {
   int mixed_c;
   bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
+// An instantiated graph is shared between the cache and every caller that is
+// about to launch it: the exec is destroyed only when the last owner lets go
+// (cache eviction / drop_graphs and an in-flight launcher can race).
+using GraphExecPtr = std::shared_ptr<CUgraphExec_st>;
+GraphExecPtr own_exec(cudaGraphExec_t e);
 struct GraphEntry {
   GraphKey key;
   int hits = 0;
-  cudaGraphExec_t exec = nullptr;
+  GraphExecPtr exec;
 };
 extern std::mutex g_graph_mu;
 extern std::vector<GraphEntry> g_graphs;
@@ -85,29 +91,26 @@ int run_graphed(const GraphKey& key, cudaStream_t s, Fn&& fn) {
     cudaGetLastError();
     return fn(s);
   }
-  cudaGraphExec_t exec = nullptr;
+  GraphExecPtr exec;
   bool capture = false;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
     auto it = std::find_if(g_graphs.begin(), g_graphs.end(),
                            [&](const GraphEntry& e) { return e.key == key; });
     if (it == g_graphs.end()) {
-      if (g_graphs.size() >= 64) {
-        if (g_graphs.front().exec) cudaGraphExecDestroy(g_graphs.front().exec);
-        g_graphs.erase(g_graphs.begin());
-      }
+      if (g_graphs.size() >= 64) g_graphs.erase(g_graphs.begin());  // FIFO eviction
       GraphEntry e;
       e.key = key;
       e.hits = 1;
       g_graphs.push_back(e);
     } else {
-      exec = it->exec;
-      capture = exec == nullptr;
+      exec = it->exec;  // shared ownership: eviction cannot free it under us
+      capture = !exec;
       ++it->hits;
     }
   }
-  if (exec == nullptr && !capture) return fn(s);  // first sighting: launch directly
-  if (exec == nullptr) {
+  if (!exec && !capture) return fn(s);  // first sighting: launch directly
+  if (!exec) {
     cudaStream_t& cs = t_capture_stream[key.dev & 63];
     if (cs == nullptr) B200_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     B200_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -119,22 +122,19 @@ int run_graphed(const GraphKey& key, cudaStream_t s, Fn&& fn) {
       return rc;
     }
     if (e != cudaSuccess) return cuda_fail(e, "graph capture");
-    e = cudaGraphInstantiateWithFlags(&exec, g, 0);
+    cudaGraphExec_t raw = nullptr;
+    e = cudaGraphInstantiateWithFlags(&raw, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+    exec = own_exec(raw);
     std::lock_guard<std::mutex> lk(g_graph_mu);
     auto it = std::find_if(g_graphs.begin(), g_graphs.end(),
                            [&](const GraphEntry& x) { return x.key == key; });
-    if (it != g_graphs.end() && it->exec == nullptr) {
-      it->exec = exec;
-    } else {
-      // another thread won the race: launch ours once, keep theirs
-      cudaError_t le = cudaGraphLaunch(exec, s);
-      cudaGraphExecDestroy(exec);
-      return le == cudaSuccess ? B200_OK : cuda_fail(le, "graph launch");
-    }
+    if (it != g_graphs.end() && !it->exec) it->exec = exec;
+    // else: another thread won the race (or the entry was evicted); ours is
+    // launched once below and freed with its last owner
   }
-  B200_CUDA_TRY(cudaGraphLaunch(exec, s));
+  B200_CUDA_TRY(cudaGraphLaunch(exec.get(), s));
   return B200_OK;
 }
 

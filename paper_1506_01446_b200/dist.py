@@ -302,6 +302,13 @@ def partitioned_sort_(shard: torch.Tensor, descending: bool = False, group=None,
     keys this rank sent per step.  ``rank``/``world`` override the process
     group's (in-process emulation of the ranks in tests).
     """
+    from . import ConfigError
+    if shard.dtype not in (torch.int32, torch.uint32):
+        raise ConfigError(f"partitioned_sort_ takes int32 or uint32 shards, got {shard.dtype}")
+    if not shard.is_contiguous() or shard.dim() != 1:
+        raise ConfigError("the shard must be a contiguous 1-D tensor")
+    if ops is None and not shard.is_cuda:
+        raise ConfigError("the shard must be a CUDA tensor (CPU ops are test-only)")
     if exchange is None:
         exchange = ("peer" if shard.is_cuda and dist.is_initialized()
                     and dist.get_backend(group) == "nccl" and ops is None else "half")

@@ -83,6 +83,27 @@ int main() {
     CHECK(r.counters.global_reads == r.counters.kernel_launches << 12);
     CHECK_THROWS_AS(bitonic::gpu::execute(PlanLike{13}, keys, 4), bitonic::invalid_size_error);
     CHECK_THROWS_AS(bitonic::gpu::execute(PlanLike{12}, keys, 0), bitonic::config_error);
+    // both arguments bad: workers is checked first (engine.cpp:177-185)
+    CHECK_THROWS_AS(bitonic::gpu::execute(PlanLike{13}, keys, 0), bitonic::config_error);
+    // a plan with the reference's launches list: counters are account() of
+    // that plan (test_engine.cpp:354-370 compares them with plan totals)
+    struct StepLike {};
+    struct LaunchLike {
+      std::vector<StepLike> steps;
+    };
+    struct PlanWithLaunches {
+      unsigned k;
+      std::vector<LaunchLike> launches;
+    };
+    PlanWithLaunches pl{12, {LaunchLike{std::vector<StepLike>(1)},
+                             LaunchLike{std::vector<StepLike>(2)},
+                             LaunchLike{std::vector<StepLike>(9)}}};
+    const auto r2 = bitonic::gpu::execute(pl, keys, 2);
+    CHECK(r2.keys == expected);
+    CHECK(r2.counters.kernel_launches == 3);
+    CHECK(r2.counters.global_reads == 3u << 12);
+    CHECK(r2.counters.global_writes == 3u << 12);
+    CHECK(r2.counters.compare_exchanges == (std::uint64_t{1} << 11) * 12);
   }
   {
     std::vector<std::int32_t> odd(6);

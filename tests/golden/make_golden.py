@@ -98,11 +98,45 @@ def main():
     for k in range(1, 33):
         r, c = ref.predicted_counts(k)
         out["counts"].append({"k": k, "rounds": r, "compare_exchanges": c})
+    out["large"] = large_cases(ref)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", path)
 
 
+def large_cases(ref):
+    """Digests at north_star's upper sizes: 2^24 through the reference's
+    sequential_bitonic_sort, 2^28 through reference_quicksort (the bitonic
+    network would take minutes on one core; any correct sort of payload-free
+    keys gives the same bytes)."""
+    cases = []
+    for k, how in [(24, "sequential_bitonic_sort"), (28, "reference_quicksort")]:
+        x = ref.generate_input(1 << k, 1)
+        u = x.view(np.uint32)
+        sort = ref.sequential_bitonic_sort if how == "sequential_bitonic_sort" else ref.quicksort
+        i32 = sort(x)
+        u32 = sort((u ^ FLIP).view(np.int32)).view(np.uint32) ^ FLIP
+        cases.append({"k": k, "seed": 1, "reference_function": how,
+                      "input_fnv": "%016x" % fnv(u),
+                      "i32_asc_fnv": "%016x" % fnv(i32),
+                      "u32_asc_fnv": "%016x" % fnv(u32),
+                      "u32_desc_fnv": "%016x" % fnv(u32[::-1].copy()),
+                      "u32_first": "%08x" % u32[0], "u32_last": "%08x" % u32[-1],
+                      "u32_median": "%08x" % u32[u32.size // 2]})
+        print("large case", k, "done", flush=True)
+    return cases
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--large-only"]:
+        # add / refresh only the large digests in the existing fixture
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
+        with open(path) as f:
+            cur = json.load(f)
+        cur["large"] = large_cases(oracle.reference())
+        with open(path, "w") as f:
+            json.dump(cur, f, indent=1)
+        print("updated", path)
+    else:
+        main()

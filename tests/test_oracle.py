@@ -176,3 +176,12 @@ def test_reference_zero_one_and_counts(ref, orc):
         assert ref.check_zero_one(k)
     for k in range(1, 30):
         assert ref.predicted_counts(k) == orc.predicted_counts(k)
+
+
+def test_oracle_at_2_24_matches_reference_digest(orc, golden):
+    """The large fixture (reference sequential_bitonic_sort at 2^24) pins the
+    oracle's generator and sort at the top of the CPU-checkable range."""
+    c = [c for c in golden["large"] if c["k"] == 24][0]
+    x = orc.generate_input(1 << 24, 1)
+    assert h(orc.fnv1a64(x)) == c["input_fnv"]
+    assert h(orc.fnv1a64(orc.quicksort_u32(x))) == c["u32_asc_fnv"]

@@ -6,7 +6,14 @@ import json
 
 import pytest
 
-from paper_1506_01446_b200 import table1 as t1
+import importlib.util
+import os
+
+_spec = importlib.util.spec_from_file_location(
+    "table1", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "tools", "table1.py"))
+t1 = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(t1)
 
 
 def test_parse_sizes_like_the_reference():

@@ -20,7 +20,10 @@ Formats follow the reference's emit_report (bench.cpp:185-290): an aligned
 table, RFC-4180 CSV with one header row, or a JSON array.  The size grammar is
 the reference's parse_sizes (bench.cpp:460-484): ``8,2^4,2^17..2^24``.
 
-    python -m paper_1506_01446_b200.table1 --sizes 2^17..2^24 --format csv
+    python tools/table1.py --sizes 2^17..2^24 --format csv
+
+A report tool beside bench.py (it times the reference's CPU code through the
+oracle/_ref checker), kept outside the product package.
 """
 from __future__ import annotations
 
@@ -32,6 +35,9 @@ import math
 import sys
 import time
 from typing import Dict, List, Optional
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 MAX_LOG2 = 48  # kMaxLog2Length, schedule.hpp:15
 
