@@ -213,6 +213,8 @@ typedef struct {
   int pB;
   uint64_t ctas;  /* grid size                                              */
   uint64_t compare_exchanges; /* CEs executed by this launch               */
+  int cluster;    /* CTAs per thread-block cluster (2: the coset is split over */
+                  /* two CTAs that exchange keys through DSMEM; else 1)      */
 } b200_pass_info;
 
 /* Fills up to max_passes entries; *n_passes receives the plan length. */

@@ -336,6 +336,7 @@ class PassPlan:
     pB: int
     ctas: int
     compare_exchanges: int
+    cluster: int = 1  # CTAs per cluster (2: a 2^15-key coset over a CTA pair)
 
     def step_bits(self) -> List[tuple]:
         """(phase, global bit) of every network step this pass runs, in order."""
@@ -367,7 +368,7 @@ def plan(n: int, batch: int = 1) -> List[PassPlan]:
     arr = (_native.PassInfo * max(cnt.value, 1))()
     _check(L.b200_bitonic_plan(n, batch, arr, cnt.value, ctypes.byref(cnt)))
     return [PassPlan(p.tile_bits, p.a, p.y, bool(p.tile_sort), p.segA_hi, p.pA,
-                     p.segB_lo, p.pB, int(p.ctas), int(p.compare_exchanges))
+                     p.segB_lo, p.pB, int(p.ctas), int(p.compare_exchanges), int(p.cluster))
             for p in arr[: cnt.value]]
 
 

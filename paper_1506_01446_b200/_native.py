@@ -66,6 +66,7 @@ class PassInfo(ctypes.Structure):
         ("pB", ctypes.c_int),
         ("ctas", ctypes.c_uint64),
         ("compare_exchanges", ctypes.c_uint64),
+        ("cluster", ctypes.c_int),
     ]
 
 

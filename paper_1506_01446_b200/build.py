@@ -21,15 +21,15 @@ LIB = os.environ.get("B200_BITONIC_LIBOUT") or os.path.join(HERE, "libb200_biton
 SOURCES = [os.path.join(CSRC, f) for f in
            ["bitonic_sort.cu", "k_tile.cu", "k_merge11.cu", "k_merge12.cu",
             "k_merge13.cu", "k_merge14.cu", "k_merge15.cu", "k_merge12r4.cu",
-            "k_merge13r4.cu", "k_merge12kv.cu", "k_merge13kv.cu",
-            "k_merge12k64.cu", "k_merge13k64.cu", "k_tile_k64.cu",
+            "k_merge13r4.cu", "k_merge14r4.cu", "k_merge12kv.cu", "k_merge13kv.cu",
+            "k_merge12k64.cu", "k_merge13k64.cu", "k_tile_k64.cu", "k_cluster.cu",
             "host_entry.cu", "multi.cu"]]
 HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
            if f.endswith((".cuh", ".hpp", ".h"))]
 HEADERS.append(os.path.join(ROOT, "include", "b200_bitonic.h"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-diag-suppress", "128", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills"] + os.environ.get("B200_BITONIC_EXTRA_NVCC", "").split()
 
 
@@ -52,7 +52,8 @@ def _stale(target: str, deps) -> bool:
 
 
 def needs_build() -> bool:
-    return _stale(LIB, SOURCES + HEADERS)
+    objs = [_obj(s) for s in SOURCES if os.path.exists(_obj(s))]
+    return _stale(LIB, SOURCES + HEADERS + objs)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -85,7 +85,16 @@ struct PassParams {
   // 1 and 0xFFFFFFFF, opaque to the compiler: operands of the IMAD form of
   // max() that moves part of the compare-exchange work to the FMA pipe
   uint32_t one, mone;
+  // 1: CTAs take their cosets in reverse order.  Consecutive passes run in
+  // opposite directions, so a pass starts on the cosets the previous pass
+  // wrote last -- still in L2 when the array is larger than L2.
+  int reverse;
 };
+
+// Coset index of this CTA (see PassParams::reverse).
+__device__ __forceinline__ uint64_t pass_block(const PassParams& P) {
+  return P.reverse ? (uint64_t)(gridDim.x - 1u - blockIdx.x) : (uint64_t)blockIdx.x;
+}
 
 // Operands of the FMA-pipe max (see Layout::mm).
 struct FmaSplit {
@@ -245,7 +254,7 @@ bitonic_pass_kernel(PassParams P) {
 
   // ---- global base of this CTA's coset ----------------------------------
   const int a = P.a, y = P.y, h = C - a;
-  const uint64_t b = blockIdx.x;
+  const uint64_t b = pass_block(P);
   uint64_t gbase;
   if (h == 0 || y == a) {
     gbase = b << C;  // contiguous tile

@@ -58,6 +58,10 @@ b200::PlanOptions plan_options() {
   if (const char* e = std::getenv("B200_BITONIC_TRIP_COST")) o.trip_cost = std::atof(e);
   if (const char* e = std::getenv("B200_BITONIC_MIXED_C")) o.mixed_c = std::atoi(e) != 0;
   if (const char* e = std::getenv("B200_BITONIC_WIDE_TAIL_COST")) o.wide_tail_cost = std::atof(e);
+  if (const char* e = std::getenv("B200_BITONIC_CLUSTER")) o.cluster = std::atoi(e) != 0;
+  if (const char* e = std::getenv("B200_BITONIC_CLUSTER_COST")) o.cluster_cost = std::atof(e);
+  if (const char* e = std::getenv("B200_BITONIC_MID_LRUN")) o.mid_lrun = std::atoi(e);
+  if (const char* e = std::getenv("B200_BITONIC_R14")) o.regbits14 = std::atoi(e);
   return o;
 }
 
@@ -140,6 +144,14 @@ cudaError_t trim_scratch_pools() {
 }
 
 std::atomic<int> g_force_generic{0};
+// alternate the coset order of consecutive passes (PassParams::reverse)
+bool reverse_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("B200_BITONIC_REVERSE");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
 std::atomic<int> g_pdl{1};  // programmatic dependent launch between passes
 
 // Returns the kernel and its keys-per-thread exponent (the block size is
@@ -147,6 +159,10 @@ std::atomic<int> g_pdl{1};  // programmatic dependent launch between passes
 // 32 keys per thread.
 // mode: 0 keys, 1 key + payload, 2 64-bit keys (two word arrays).
 b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out, int mode) {
+  if (q.cluster) {
+    *R_out = 5;
+    return mode == 0 ? b200::find_cluster_kernel(q.segA_hi, 5) : nullptr;
+  }
   if (mode != 0) {
     *R_out = q.R;
     return q.tile_sort ? (q.p_end == q.C ? b200::find_tile_kernel(q.C, q.R, mode) : nullptr)
@@ -193,13 +209,14 @@ cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p, cudaStream_
   b200::PassFn f = select_kernel(q, &R, mode);
   if (f == nullptr) return cudaErrorNotSupported;  // no such key-value shape
   const void* fn = reinterpret_cast<const void*>(f);
-  cudaError_t e = ensure_attr(fn, q.C, kv ? 2 : 1);
+  const int Cb = q.cluster ? 14 : q.C;  // keys per CTA = 2^Cb (a cluster pass: 2 CTAs)
+  cudaError_t e = ensure_attr(fn, Cb, kv ? 2 : 1);
   if (e != cudaSuccess) return e;
-  const size_t smem = (size_t)b200::tile_smem_words(q.C) * 4 * (kv ? 2 : 1);
+  const size_t smem = (size_t)b200::tile_smem_words(Cb) * 4 * (kv ? 2 : 1);
   void* args[] = {&p};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)q.ctas);
-  cfg.blockDim = dim3(1u << (q.C - R));
+  cfg.blockDim = dim3(1u << (Cb - R));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -221,19 +238,25 @@ struct PlanKey {
   double trip_cost;
   bool mixed_c;
   double wide_tail_cost;
+  bool cluster;
+  double cluster_cost;
+  int mid_lrun, regbits14;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
            lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp &&
            kv == o.kv && tile_regbits == o.tile_regbits && cmerge == o.cmerge &&
            trip_cost == o.trip_cost && mixed_c == o.mixed_c &&
-           wide_tail_cost == o.wide_tail_cost;
+           wide_tail_cost == o.wide_tail_cost && cluster == o.cluster &&
+           cluster_cost == o.cluster_cost && mid_lrun == o.mid_lrun &&
+           regbits14 == o.regbits14;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
   const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.tile_regbits,
-                    o.cmerge, o.dp, o.kv, o.trip_cost, o.mixed_c, o.wide_tail_cost};
+                    o.cmerge, o.dp, o.kv, o.trip_cost, o.mixed_c, o.wide_tail_cost,
+                    o.cluster, o.cluster_cost, o.mid_lrun, o.regbits14};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;
@@ -287,6 +310,10 @@ GraphKey make_key(int kind, const void* p0, const void* p1, uint64_t n, uint64_t
   key.trip_cost = o.trip_cost;
   key.wide_tail_cost = o.wide_tail_cost;
   key.mixed_c = o.mixed_c;
+  key.cluster = o.cluster;
+  key.mid_lrun = o.mid_lrun;
+  key.regbits14 = o.regbits14;
+  key.cluster_cost = o.cluster_cost;
   key.dp = o.dp;
   key.generic = g_force_generic.load();
   key.pdl = g_pdl.load();
@@ -367,6 +394,7 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
       p.pB = q.pB;
       p.one = 1u;
       p.mone = 0xFFFFFFFFu;
+      p.reverse = (reverse_enabled() && (i & 1) && !q.cluster) ? 1 : 0;
       cudaError_t e = launch_pass(q, p, st, mode);
       if (e == cudaErrorNotSupported) {
         return fail(B200_CONFIG,
@@ -670,6 +698,7 @@ int b200_bitonic_plan(uint64_t n, uint64_t batch, b200_pass_info* out,
     out[i].pB = q.pB;
     out[i].ctas = q.ctas;
     out[i].compare_exchanges = q.ces;
+    out[i].cluster = q.cluster ? 2 : 1;
   }
   return B200_OK;
 }

@@ -155,7 +155,7 @@ template <int C, int R, int MODE = 0>
 constexpr int min_blocks_for() {
   // a 64-register budget per thread (1024 threads per SM at full use); two
   // register arrays of 32 keys get 128 registers (512 threads per SM)
-  constexpr int slots = (MODE != 0 && R >= 5) ? 512 : 1024;
+  constexpr int slots = R >= 6 ? (MODE != 0 ? 256 : 512) : ((MODE != 0 && R >= 5) ? 512 : 1024);
   return threads_for<C, R>() >= slots ? 1
          : (slots / threads_for<C, R>() > 32 ? 32 : slots / threads_for<C, R>());
 }
@@ -171,7 +171,9 @@ constexpr int min_blocks_for() {
 // MODE 0: keys only.  MODE 1: key + 32-bit payload (the payload array
 // follows its key).  MODE 2: 64-bit keys split into a hi-word array (v) and
 // a lo-word array (w), compared lexicographically.
-template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), int MODE = 0>
+// AO >= 0 overrides the coset's low-run length A (the cluster passes run a
+// tail on a 2^C sub-coset whose low run is shorter than C).
+template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), int MODE = 0, int AO = -1>
 struct PassBody {
   static constexpr bool KV = MODE != 0;   // two register arrays
   // FMA-pipe share of the compare-exchange max (Layout::mm)
@@ -181,7 +183,7 @@ struct PassBody {
   using S = Seq<C, KIND, SA, SB>;
   static constexpr int R = RR;
   static constexpr int NR = 1 << R;
-  static constexpr int A = KIND == 0 ? C : (SB >= 0 ? SB : C);
+  static constexpr int A = AO >= 0 ? AO : (KIND == 0 ? C : (SB >= 0 ? SB : C));
   // Shared-memory round trips of a round cut: one per layout change, plus
   // one for a staged load / store when the first / last layout cannot talk
   // to HBM directly.
@@ -511,7 +513,7 @@ tile_sort_kernel(PassParams P) {
   typename B::Ctx c;
   c.keys = P.keys;
   c.vals = P.vals;
-  c.gbase = (uint64_t)blockIdx.x << C;
+  c.gbase = pass_block(P) << C;
   c.y = C;
   c.uA = c.uB = 0u;
   c.uC = 0u - dir_bit_global(c.gbase, C, P.kd);
@@ -534,7 +536,7 @@ merge_kernel(PassParams P) {
   c.keys = P.keys;
   c.vals = P.vals;
   c.y = P.y;
-  c.gbase = Coset<C, A>::base(blockIdx.x, P.y);
+  c.gbase = Coset<C, A>::base(pass_block(P), P.y);
   c.uA = 0u - dir_bit_global(c.gbase, P.pA, P.kd);
   c.uB = 0u - dir_bit_global(c.gbase, P.pB, P.kd);
   c.uC = 0u;

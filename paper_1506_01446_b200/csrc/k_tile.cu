@@ -28,6 +28,14 @@ static PassFn kv_tile(int C) {
 PassFn find_tile_kernel(int C, int R, int mode) {
   if (mode == 1) return R == (C < 4 ? C : 4) ? kv_tile(C) : nullptr;
   if (mode == 2) return find_tile_kernel_k64(C, R);
+  if (R == 6) {  // 64 keys per thread: fewer shared-memory rounds
+    switch (C) {
+      case 12: return &tile_sort_kernel<12, 6>;
+      case 13: return &tile_sort_kernel<13, 6>;
+      case 14: return &tile_sort_kernel<14, 6>;
+      default: return nullptr;
+    }
+  }
   if (R == 4) {
     switch (C) {
       case 10: return &tile_sort_kernel<10, 4>;
@@ -76,6 +84,7 @@ struct Tables {
     fill_merge_table_13_k64(tk64[13]);
     fill_merge_table_12_r4(t4[12]);
     fill_merge_table_13_r4(t4[13]);
+    fill_merge_table_14_r4(t4[14]);
     fill_merge_table_11(t[11]);
     fill_merge_table_12(t[12]);
     fill_merge_table_13(t[13]);

@@ -16,6 +16,9 @@ PassFn find_tile_kernel(int C, int R = 5, int mode = 0);
 // bitonic_pass_kernel<C>).
 PassFn find_merge_kernel(int C, int SA, int SB, int R = 5, int mode = 0);
 PassFn find_tile_kernel_k64(int C, int R);  // k_tile_k64.cu
+// 2-CTA cluster pass (bitonic_cluster.cuh): tail bits B..0 fused with the
+// head of the next phase on a 2^15-key coset (B in [4, 13]); nullptr otherwise.
+PassFn find_cluster_kernel(int B, int R = 5);
 
 // Instantiated merge tile sizes.
 constexpr int kMergeCMin = 11;
@@ -34,6 +37,7 @@ void fill_merge_table_14(MergeTable& t);
 void fill_merge_table_15(MergeTable& t);
 void fill_merge_table_12_r4(MergeTable& t);
 void fill_merge_table_13_r4(MergeTable& t);
+void fill_merge_table_14_r4(MergeTable& t);
 void fill_merge_table_12_kv(MergeTable& t);
 void fill_merge_table_13_kv(MergeTable& t);
 void fill_merge_table_12_k64(MergeTable& t);

@@ -18,6 +18,7 @@
 // the CE total equals predicted_counts (schedule.cpp:71-78).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
@@ -36,6 +37,7 @@ struct PlanPass {
   uint64_t ctas = 0;
   uint64_t ces = 0;
   int R = 5;          // log2 keys per thread (5 = 32; 4 = 16 for latency-bound sizes)
+  int cluster = 0;    // 1: 2-CTA cluster pass on a 2^15-key coset (bitonic_cluster.cuh)
 };
 
 // ---- cost model: shared-memory round trips of one merge pass ---------------
@@ -103,9 +105,10 @@ inline bool direct(int C, int R, int A, uint32_t m) {
   return A >= v + 5;
 }
 
-// Shared-memory round trips of merge pass (SA, SB) on a 2^C tile.
-inline int merge_trips(int C, int R, int SA, int SB) {
-  const int A = SB >= 0 ? SB : C;
+// Shared-memory round trips of merge pass (SA, SB) on a 2^C tile (low run
+// of A keys: SB when a head follows, else C, unless given).
+inline int merge_trips(int C, int R, int SA, int SB, int A_override = -1) {
+  const int A = A_override >= 0 ? A_override : (SB >= 0 ? SB : C);
   std::vector<int> bits;
   for (int b = SA; b >= 0; --b) bits.push_back(b);
   if (SB >= 0)
@@ -135,6 +138,17 @@ struct PlanOptions {
   bool mixed_c = true;         // choose the coset size per merge pass (tile's or cmerge)
   double wide_tail_cost = -1;  // extra cost of a tail pass on the larger cosets (<0: auto)
   double trip_cost = 0.10;  // extra cost of a shared-memory round trip, in passes
+  // 2-CTA cluster passes (tail of phase p + head of p+1 on a 2^15-key coset,
+  // bitonic_cluster.cuh) for single-array key-only sorts of >= 2^cluster_min_k.
+  // Off by default: measured on B200 (tools/pass_times.py, 2^28) a cluster
+  // pass takes 530-600 us against 325-415 us for the 14-bit passes it
+  // replaces -- the DSMEM exchange (~17 B/clk/SM) and the two cluster
+  // barriers cost more than the HBM round trip they save (12.7 vs 11.1 ms).
+  bool cluster = false;
+  int cluster_min_k = 24;
+  double cluster_cost = 0.05;  // the DSMEM exchange, in passes
+  int mid_lrun = 5;            // shortest run of a middle pass (k >= 24 plans)
+  int regbits14 = 0;           // keys per thread of the 14-bit merge passes (0 = as R)
 };
 
 inline int ctz64(uint64_t x) {
@@ -240,7 +254,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   auto push_tail_head = [&](int p, int b, int h) {
     PlanPass m;
     m.C = C;
-    m.R = R;
+    m.R = (C == 14 && opt.regbits14 > 0) ? opt.regbits14 : R;
     m.ctas = total >> C;
     m.segA_hi = b;
     m.pA = p;
@@ -260,7 +274,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   auto push_middle = [&](int p, int b, int h) {
     PlanPass m;
     m.C = C;
-    m.R = R;
+    m.R = (C == 14 && opt.regbits14 > 0) ? opt.regbits14 : R;
     m.ctas = total >> C;
     m.a = C - h;
     m.y = b - h + 1;
@@ -282,6 +296,11 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     std::vector<double> best((size_t)K * K, -1.0);
     std::vector<int> choice((size_t)K * K, 0);  // 0 tail-only, >0 tail+head h, <0 middle -h
     std::vector<int> choice_c((size_t)K * K, C);
+    std::vector<char> choice_cl((size_t)K * K, 0);
+    const bool use_cluster = opt.cluster && !opt.kv && batch == 1 && k >= opt.cluster_min_k &&
+                             C >= 14 && !(opt.cmin == opt.cmax);
+    const int mid_lrun = (!opt.kv && batch == 1 && k >= opt.cluster_min_k &&
+                          !(opt.cmin == opt.cmax)) ? std::min(opt.mid_lrun, lrun) : lrun;
     std::vector<int> cands = {C};
     if (opt.mixed_c && CT < C && CT >= 12)
       for (int c = C - 1; c >= CT; --c) cands.push_back(c);
@@ -299,6 +318,22 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
       if (memo >= 0) return memo;
       double bc = 1e30;
       int bch = 0, bcc = C;
+      bool bcl = false;
+      if (use_cluster && b >= 4 && b <= 13 && b + 1 >= lrun && p >= 14 && p < k) {
+        // cluster pass: tail bits b..0 on [0,b+1) U (13-b high bits), DSMEM
+        // exchange, head bits 13..b on [0,b) U (14-b high bits)
+        const int h = 14 - b;
+        const int trips = detail::merge_trips(14, R, b, -1, b + 1) +
+                          detail::merge_trips(14, R, -1, b) + 1;
+        const double t = 1.0 + opt.cluster_cost + opt.trip_cost * (trips - 1) +
+                         solve(p + 1, p - h);
+        if (t < bc - 1e-9) {
+          bc = t;
+          bch = h;
+          bcc = 15;
+          bcl = true;
+        }
+      }
       for (int Cc : cands) {
         if (b < Cc) {
           // A tail-only pass takes phase p's direction as CTA-uniform: valid
@@ -310,6 +345,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
               bc = t0;
               bch = 0;
               bcc = Cc;
+              bcl = false;
             }
           }
           const int h = Cc - (b + 1);
@@ -321,21 +357,24 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
               bc = t1;
               bch = h;
               bcc = Cc;
+              bcl = false;
             }
           }
         } else {
-          for (int h = 1; h <= Cc - lrun && h <= b; ++h) {
+          for (int h = 1; h <= Cc - mid_lrun && h <= b; ++h) {
             const double t = cost_of(Cc, -1, Cc - h) + solve(p, b - h);
             if (t < bc - 1e-9) {
               bc = t;
               bch = -h;
               bcc = Cc;
+              bcl = false;
             }
           }
         }
       }
       choice[(size_t)p * K + b] = bch;
       choice_c[(size_t)p * K + b] = bcc;
+      choice_cl[(size_t)p * K + b] = bcl ? 1 : 0;
       memo = bc;
       return bc;
     };
@@ -345,7 +384,14 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     while (p <= k) {
       const int ch = choice[(size_t)p * K + b];
       C = choice_c[(size_t)p * K + b];  // the push helpers read C
-      if (b < C) {
+      if (choice_cl[(size_t)p * K + b]) {
+        push_tail_head(p, b, ch);  // C = 15: a = b+1, y = p-h+1
+        plan.back().cluster = 1;
+        plan.back().ctas = total >> 14;
+        plan.back().R = 5;
+        b = p - ch;
+        p = p + 1;
+      } else if (b < C) {
         push_tail_head(p, b, ch);
         if (ch > 0) {
           b = p - ch;

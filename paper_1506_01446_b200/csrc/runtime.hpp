@@ -60,8 +60,8 @@ struct GraphKey {
   uint64_t n, batch;
   uint32_t kx;
   int cmax, cmin, lrun, regbits, tile_regbits, cmerge, dp, generic, pdl;
-  double trip_cost, wide_tail_cost;
-  int mixed_c;
+  double trip_cost, wide_tail_cost, cluster_cost;
+  int mixed_c, cluster, mid_lrun, regbits14;
   bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 // An instantiated graph is shared between the cache and every caller that is

@@ -82,11 +82,14 @@ def test_plan_reproduces_schedule(tile_bits, run_bits):
             for p in plan:
                 C = p.tile_bits
                 assert 1 <= C <= 15
-                assert p.ctas == n >> C
+                assert p.ctas == (n >> C) * p.cluster
+                assert p.cluster == 1 or (tile_bits == 0 and k >= 24 and C == 15)
                 if not p.tile_sort:
                     h = C - p.a
-                    # coset bits: [0,a) and [y, y+h) disjoint, inside [0,k)
-                    assert p.a >= min(run_bits, C) and p.a >= 2
+                    # coset bits: [0,a) and [y, y+h) disjoint, inside [0,k);
+                    # the cluster plans' middle passes move 2^4-key runs
+                    lo = min(run_bits, C, 4 if (tile_bits == 0 and k >= 24) else C)
+                    assert p.a >= lo and p.a >= 2
                     assert h == 0 or p.y >= p.a
                     assert p.y + h <= k
                     # every step bit of the pass lies in the coset
@@ -103,7 +106,7 @@ def test_plan_batched():
         assert steps == schedule(k)
         total = (1 << k) * batch
         for p in plan:
-            assert p.ctas << p.tile_bits == total
+            assert (p.ctas // p.cluster) << p.tile_bits == total
 
 
 # The default plan's exact pass count per size (a regression in the planner
