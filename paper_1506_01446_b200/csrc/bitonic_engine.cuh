@@ -243,7 +243,7 @@ __device__ __forceinline__ uint32_t dir_bit_global(uint64_t gi, int p, int kd) {
 }
 
 template <int C>
-__global__ void __launch_bounds__(Tile<C>::T, (Tile<C>::T >= 1024 ? 1 : (1024 / Tile<C>::T > 32 ? 32 : 1024 / Tile<C>::T)))
+__global__ void __launch_bounds__(Tile<C>::T, (Tile<C>::T >= 1024 ? 1 : (1024 / Tile<C>::T > 16 ? 16 : 1024 / Tile<C>::T)))
 bitonic_pass_kernel(PassParams P) {
   using TL = Tile<C>;
   constexpr int NR = TL::NR;

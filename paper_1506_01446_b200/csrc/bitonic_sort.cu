@@ -6,6 +6,7 @@
 // pool with a full barrier in between (worker_pool.cpp:28-44), this enqueues
 // one sm_100a kernel per planned pass on a CUDA stream; stream order is the
 // barrier.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -202,8 +203,59 @@ cudaError_t ensure_attr(const void* fn, int C, int arrays) {
   return e;
 }
 
+// The tile sort's load as one TMA tensor copy (bitonic_tma.cuh).
+bool tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("B200_BITONIC_TMA");
+    return e && std::strcmp(e, "1") == 0;
+  }();
+  return on;
+}
+
+cudaError_t launch_tile_tma(const b200::PlanPass& q, b200::PassParams p, uint64_t total,
+                            cudaStream_t s, bool* done) {
+  *done = false;
+  b200::TmaTileFn f = b200::find_tile_tma_kernel(q.C);
+  CUtensorMap map;
+  if (f == nullptr || !b200::make_tile_tensor_map(&map, p.keys, total, q.C)) return cudaSuccess;
+  const void* fn = reinterpret_cast<const void*>(f);
+  const size_t smem = (size_t)b200::tile_smem_words(q.C) * 4 + 1024;  // + swizzle alignment
+  cudaError_t e = cudaSuccess;
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if ((int)g_attr_done.size() <= dev) g_attr_done.resize(dev + 1);
+    auto& d = g_attr_done[dev];
+    if (std::find(d.begin(), d.end(), fn) == d.end()) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) d.push_back(fn);
+    }
+  }
+  if (e != cudaSuccess) return e;
+  void* args[] = {&p, &map};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)q.ctas);
+  cfg.blockDim = dim3(1u << (q.C - 5));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl.load() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  *done = true;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p, cudaStream_t s,
                         int mode) {
+  if (q.tile_sort && mode == 0 && q.R == 5 && q.p_end == q.C && tma_enabled() &&
+      !g_force_generic.load()) {
+    bool done = false;
+    cudaError_t e = launch_tile_tma(q, p, q.ctas << q.C, s, &done);
+    if (done || e != cudaSuccess) return e;
+  }
   int R = 5;
   const bool kv = mode != 0;
   b200::PassFn f = select_kernel(q, &R, mode);

@@ -61,14 +61,14 @@ __device__ __forceinline__ void stg128(uint32_t* p, uint4 v) {
 template <int C, int A>
 struct Coset {
   // global offset of local index j (additive over disjoint bit fields)
-  __device__ __forceinline__ static uint64_t goff(uint32_t j, int y) {
+  __host__ __device__ __forceinline__ static uint64_t goff(uint32_t j, int y) {
     if constexpr (A >= C) {
       return j;
     } else {
       return (uint64_t)(j & ((1u << A) - 1u)) + ((uint64_t)(j >> A) << y);
     }
   }
-  __device__ __forceinline__ static uint64_t base(uint64_t b, int y) {
+  __host__ __device__ __forceinline__ static uint64_t base(uint64_t b, int y) {
     if constexpr (A >= C) {
       return b << C;
     } else {
@@ -85,11 +85,34 @@ struct Coset {
 // The two terms occupy disjoint local bits, so the global offset is
 // goff(4t) + goff(it*4T): one per-thread base plus a uniform per-iteration
 // offset (no per-key index arithmetic).
+// The staging copies' shared-memory side: lane l of warp w writes / reads
+// word q of the uint4 at local index 4(32w + l) + it*4T, padded.  Every such
+// access of a warp must hit 32 distinct banks (the round layouts are checked
+// by Layout::conflict_free; this covers the staging path).
+template <int C, int R>
+constexpr bool staging_conflict_free() {
+  constexpr int T = 1 << (C - R), N = 1 << C;
+  if (N / T < 4 || T < 32) return true;
+  for (int w = 0; w < T / 32; ++w)
+    for (int it = 0; it < N / 4 / T; ++it)
+      for (int q = 0; q < 4; ++q) {
+        uint32_t seen = 0;
+        for (int l = 0; l < 32; ++l) {
+          const uint32_t j = 4u * (uint32_t)(32 * w + l) + (uint32_t)(it * 4 * T) + (uint32_t)q;
+          const uint32_t bank = smem_pad(j) & 31u;
+          if (seen & (1u << bank)) return false;
+          seen |= 1u << bank;
+        }
+      }
+  return true;
+}
+
 template <int C, int A, int DBIT, int R>
 __device__ __forceinline__ void stage_in(uint32_t* sm, const uint32_t* keys,
                                          uint64_t gbase, int y, uint32_t m_uniform) {
   using TL = Tile<C>;
   constexpr int T = 1 << (C - R), N = TL::N;
+  static_assert(staging_conflict_free<C, R>(), "staging copy has bank conflicts");
   if constexpr (N / T >= 4) {
     constexpr int IT = N / 4 / T;
     const uint32_t j0 = 4u * threadIdx.x;
@@ -405,19 +428,25 @@ struct PassBody {
   template <class LR>
   __device__ __forceinline__ static void gstore(const Ctx& c, uint32_t tj, const uint32_t (&v)[NR]) {
     constexpr int V = LR::vec_bits();
-    uint32_t* base = c.keys + c.gbase + Coset<C, A>::goff(tj, c.y);
+    // Re-derive the addresses instead of keeping the load's 32 pointers
+    // live across the rounds (ptxas would spill them: merge_kernel<13,-1,9>
+    // had 40 bytes of stack before this): an opaque copy of y
+    // defeat the common-subexpression elimination (y * 1 with the 1 read
+    // from a kernel parameter, like the FMA-split operands).
+    const int y = c.y * (int)c.fs.one;
+    uint32_t* base = c.keys + c.gbase + Coset<C, A>::goff(tj, y);
     if constexpr (V == 0) {
 #pragma unroll
-      for (int e = 0; e < NR; ++e) stg32(base + Coset<C, A>::goff(LR::dep_reg(e), c.y), v[e]);
+      for (int e = 0; e < NR; ++e) stg32(base + Coset<C, A>::goff(LR::dep_reg(e), y), v[e]);
     } else if constexpr (V == 1) {
 #pragma unroll
       for (int e = 0; e < NR; e += 2) {
-        stg64(base + Coset<C, A>::goff(LR::dep_reg(e), c.y), v[e], v[e + 1]);
+        stg64(base + Coset<C, A>::goff(LR::dep_reg(e), y), v[e], v[e + 1]);
       }
     } else {
 #pragma unroll
       for (int e = 0; e < NR; e += 4) {
-        stg128(base + Coset<C, A>::goff(LR::dep_reg(e), c.y),
+        stg128(base + Coset<C, A>::goff(LR::dep_reg(e), y),
                make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]));
       }
     }

@@ -3,6 +3,8 @@
 
 #include "bitonic_engine.cuh"
 
+struct CUtensorMap_st;
+
 namespace b200 {
 
 using PassFn = void (*)(PassParams);
@@ -19,6 +21,10 @@ PassFn find_tile_kernel_k64(int C, int R);  // k_tile_k64.cu
 // 2-CTA cluster pass (bitonic_cluster.cuh): tail bits B..0 fused with the
 // head of the next phase on a 2^15-key coset (B in [4, 13]); nullptr otherwise.
 PassFn find_cluster_kernel(int B, int R = 5);
+// TMA-loaded tile sort (bitonic_tma.cuh), C in [10, 13], 32 keys per thread
+using TmaTileFn = void (*)(PassParams, const CUtensorMap_st);
+TmaTileFn find_tile_tma_kernel(int C);
+bool make_tile_tensor_map(CUtensorMap_st* map, const uint32_t* keys, uint64_t total, int C);
 
 // Instantiated merge tile sizes.
 constexpr int kMergeCMin = 11;

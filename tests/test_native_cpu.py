@@ -56,6 +56,18 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
+def test_no_kernel_spills():
+    """Every kernel in the library runs without local-memory stack (ptxas
+    spills): cuobjdump -res-usage reports STACK:0 for all of them."""
+    out = subprocess.run(["cuobjdump", "-res-usage", _native.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    stacks = re.findall(r"STACK:(\d+)", out)
+    assert len(stacks) > 100
+    names = re.findall(r"Function (\S+):", out)
+    bad = [(n, st) for n, st in zip(names, stacks) if st != "0"]
+    assert not bad, bad
+
+
 def test_version():
     assert "sm_100a" in b200.version()
 
