@@ -786,6 +786,53 @@ def main():
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "error": str(e)}
 
+    # ---- N>1: NVLink bytes and the 1-GPU time of the same total -------------
+    multi = None
+    if world > 1:
+        multi = {}
+        pk = dist_stats.pop("partner_keys", None)
+        if pk is not None:
+            per_step = [4 * int(x) for x in pk.tolist()]  # bytes this rank read over NVLink
+            t = torch.tensor(per_step, device=dev, dtype=torch.int64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            multi["nvlink_bytes_per_rank_per_step_max"] = t.tolist()
+            multi["nvlink_bytes_per_step_all_ranks"] = None
+            tsum = torch.tensor(per_step, device=dev, dtype=torch.int64)
+            dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+            multi["nvlink_bytes_per_step_all_ranks"] = tsum.tolist()
+            multi["nvlink_floor_us_per_step"] = [b / 900e9 * 1e6 for b in t.tolist()]
+            multi["nvlink_link_gbs_assumed"] = 900.0
+        # strong-scaling reference: rank 0 sorts the whole 2^k-key array alone
+        # (same kernels, one GPU), so efficiency is self-contained in the line
+        barrier()
+        if rank == 0 and not shared_gpu:
+            try:
+                del work
+                torch.cuda.empty_cache()
+                big = torch.empty(keys_total, dtype=torch.uint32, device=dev)
+                gi = torch.Generator(device=dev)
+                gi.manual_seed(SEED)
+                ts = []
+                for i in range(3):
+                    big.view(torch.int32).random_(generator=gi)
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    b200.sort_(big)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    if i:
+                        ts.append(e0.elapsed_time(e1))
+                one_ms = sum(ts) / len(ts)
+                multi["one_gpu_ms_same_total"] = one_ms
+                multi["one_gpu_gkeys_same_total"] = keys_total / (one_ms * 1e-3) / 1e9
+                multi["speedup_vs_one_gpu"] = one_ms / ms
+                del big
+                torch.cuda.empty_cache()
+            except Exception as ex:  # pragma: no cover - report, do not fail
+                multi["one_gpu_error"] = repr(ex)[:200]
+        barrier()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world,
@@ -803,6 +850,7 @@ def main():
                           if world > 1 else {})},
             "e2e": e2e, "roofline": roofline, "sort_roofline": sort_roof,
             "cpu_baseline": cpu, "clocks": sampler.summary(),
+            **({"multi_gpu": multi} if multi is not None else {}),
             "gpu_launches": launches_per_step * args.steps,
             "wall_s": wall,
         }

@@ -151,8 +151,11 @@ int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending);
  * repeat (then the "ranks" share one GPU and exchange through its memory).
  * Each rank sorts locally, then a rank-level bitonic network of merge-split
  * steps runs; the merge kernel reads the partner's shard directly through
- * CUDA peer memory (NVLink).  Synchronous.  Allocates one scratch shard per
- * rank. */
+ * CUDA peer memory (NVLink).  Synchronous (waits for prior work on the
+ * shards' devices).  One scratch shard per rank, the streams and events are
+ * kept for the next call with the same devices and size
+ * (b200_bitonic_release_scratch frees them); peer access is enabled once per
+ * device pair. */
 int b200_bitonic_sort_u32_multi(uint32_t* const* d_shards, const int* devices,
                                 int ngpu, uint64_t n_total, int descending);
 
@@ -190,6 +193,24 @@ int b200_bitonic_ipc_alloc(uint64_t bytes, void** d_ptr, b200_ipc_handle* handle
 int b200_bitonic_ipc_free(void* d_ptr);
 int b200_bitonic_ipc_open(const b200_ipc_handle* handle, void** d_ptr);
 int b200_bitonic_ipc_close(void* d_ptr);
+/* merge_split that also adds, on the stream, the number of keys of `out`
+ * taken from `partner` (the keys that crossed the link) to the device
+ * counter *d_partner_keys (may be null). */
+int b200_bitonic_merge_split_u32_count(const uint32_t* local, const uint32_t* partner,
+                                       uint64_t m, int keep_high, uint32_t key_xor,
+                                       uint32_t* out, b200_stream_t stream,
+                                       uint64_t* d_partner_keys);
+
+/* Device-side ordering between processes: interprocess CUDA events (one per
+ * rank and network step, handles exchanged once).  A rank records its event
+ * after its merge of a step; the partner's stream waits on it before its
+ * next merge -- no host synchronisation of the GPU between steps. */
+int b200_bitonic_ipc_event_create(void** event, b200_ipc_handle* handle);
+int b200_bitonic_ipc_event_open(const b200_ipc_handle* handle, void** event);
+int b200_bitonic_event_destroy(void* event);
+int b200_bitonic_event_record(void* event, b200_stream_t stream);
+int b200_bitonic_stream_wait_event(b200_stream_t stream, void* event);
+
 /* Stream-ordered device-to-device copy (moves a shard into / out of the
  * IPC buffers). */
 int b200_bitonic_copy(void* dst, const void* src, uint64_t bytes, b200_stream_t stream);

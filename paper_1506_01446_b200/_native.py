@@ -33,6 +33,12 @@ EXPORTED = (
     "b200_bitonic_ipc_open",
     "b200_bitonic_ipc_close",
     "b200_bitonic_copy",
+    "b200_bitonic_merge_split_u32_count",
+    "b200_bitonic_ipc_event_create",
+    "b200_bitonic_ipc_event_open",
+    "b200_bitonic_event_destroy",
+    "b200_bitonic_event_record",
+    "b200_bitonic_stream_wait_event",
     "b200_bitonic_sort_padded_u32",
     "b200_bitonic_sort_padded_i32",
     "b200_bitonic_sort_host_i32",
@@ -99,6 +105,12 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_ipc_open.argtypes = [ctypes.POINTER(IpcHandle), ctypes.POINTER(vp)]
     L.b200_bitonic_ipc_close.argtypes = [vp]
     L.b200_bitonic_copy.argtypes = [vp, vp, u64, vp]
+    L.b200_bitonic_merge_split_u32_count.argtypes = [vp, vp, u64, i, ctypes.c_uint32, vp, vp, vp]
+    L.b200_bitonic_ipc_event_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(IpcHandle)]
+    L.b200_bitonic_ipc_event_open.argtypes = [ctypes.POINTER(IpcHandle), ctypes.POINTER(vp)]
+    L.b200_bitonic_event_destroy.argtypes = [vp]
+    L.b200_bitonic_event_record.argtypes = [vp, vp]
+    L.b200_bitonic_stream_wait_event.argtypes = [vp, vp]
     L.b200_bitonic_sort_pairs_u32.argtypes = [vp, vp, u64, i, vp]
     L.b200_bitonic_sort_pairs_i32.argtypes = [vp, vp, u64, i, vp]
     L.b200_bitonic_sort_pairs_u32_batched.argtypes = [vp, vp, u64, u64, i, vp]

@@ -52,8 +52,27 @@ def _stale(target: str, deps) -> bool:
 
 
 def needs_build() -> bool:
-    objs = [_obj(s) for s in SOURCES if os.path.exists(_obj(s))]
-    return _stale(LIB, SOURCES + HEADERS + objs)
+    if not all(os.path.exists(_obj(s)) for s in SOURCES):
+        return True
+    return _stale(LIB, SOURCES + HEADERS + [_obj(s) for s in SOURCES])
+
+
+# The race-stress variant (-DB200_JITTER: random sleeps at every shared-
+# memory hand-off, bitonic_static.cuh jitter()) used by tests/test_gpu_jitter.py.
+JITTER_OBJ = os.path.join(ROOT, "build", "obj_jitter")
+JITTER_LIB = os.path.join(HERE, "libb200_bitonic_jitter.so")
+
+
+def build_jitter(verbose: bool = False) -> str:
+    global OBJ, LIB
+    saved = (OBJ, LIB, list(NVCC_FLAGS))
+    OBJ, LIB = JITTER_OBJ, JITTER_LIB
+    NVCC_FLAGS.append("-DB200_JITTER")
+    try:
+        return build(verbose=verbose)
+    finally:
+        OBJ, LIB = saved[0], saved[1]
+        NVCC_FLAGS[:] = saved[2]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -140,13 +140,16 @@ struct ClusterPass {
     const uint32_t m = c1.uA ^ c2.uB;
 #pragma unroll
     for (int e = 0; e < NR; ++e) v[e] ^= m;
+    jitter(5);
     LL::sts(sm, v);
     cluster_arrive();  // this CTA's keys are in its shared memory ...
     cluster_wait();    // ... and so are the peer's
+    jitter(6);
     exchange_load(sm, c, v);
     cluster_arrive();  // done reading both CTAs' shared memory
     B2::template steps<0, B2::RD::begin(0)>(c2, v, w);
     cluster_wait();    // the peer has read ours: shared memory may be reused
+    jitter(7);
     B2::template rounds<1>(c2, sm, v, w);
     B2::store(c2, sm, v, w);
     pdl_trigger();

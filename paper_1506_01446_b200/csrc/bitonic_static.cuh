@@ -57,6 +57,25 @@ __device__ __forceinline__ void stg128(uint32_t* p, uint4 v) {
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
+// ---- race stress (test builds only) ------------------------------------------
+// With -DB200_JITTER every shared-memory hand-off point first sleeps a
+// pseudo-random 0..1023 ns (per lane, per call site, per CTA, per clock), so
+// the relative timing of threads, warps and CTAs differs from any production
+// run; a missing barrier would surface as wrong output in the tests run
+// against this build (tests/test_gpu_jitter.py).  No-op otherwise.
+__device__ __forceinline__ void jitter(uint32_t site) {
+#ifdef B200_JITTER
+  uint32_t h = (blockIdx.x * 0x9E3779B9u) ^ (threadIdx.x * 0x85EBCA6Bu) ^ (site * 0xC2B2AE35u) ^
+               (uint32_t)clock();
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep((h >> 20) & 1023u);
+#else
+  (void)site;
+#endif
+}
+
 // ---- coset geometry ----------------------------------------------------------
 template <int C, int A>
 struct Coset {
@@ -122,6 +141,7 @@ __device__ __forceinline__ void stage_in(uint32_t* sm, const uint32_t* keys,
     for (int it = 0; it < IT; ++it) {
       buf[it] = ldg128(base + Coset<C, A>::goff((uint32_t)(it * 4 * T), y));
     }
+    jitter(1);
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const uint32_t j = j0 + (uint32_t)(it * 4 * T);
@@ -148,7 +168,9 @@ __device__ __forceinline__ void stage_out(const uint32_t* sm, uint32_t* keys,
                                           uint64_t gbase, int y) {
   using TL = Tile<C>;
   constexpr int T = 1 << (C - R), N = TL::N;
+  jitter(2);
   __syncthreads();
+  jitter(3);
   if constexpr (N / T >= 4) {
     constexpr int IT = N / 4 / T;
     const uint32_t j0 = 4u * threadIdx.x;
@@ -496,6 +518,7 @@ struct PassBody {
         gstore<LL>(cv, tj, w);
       }
     } else {
+      jitter(4);
       LL::sts(sm, v);
       if constexpr (KV) LL::sts(sm + TW, w);
       stage_out<C, A, R>(sm, c.keys, c.gbase, c.y);
@@ -508,6 +531,7 @@ struct PassBody {
                                                 uint32_t (&w)[NR]) {
     if constexpr (r < NRND) {
       if constexpr (r > 0) {
+        jitter(10 + 2 * r);
         L<r - 1>::sts(sm, v);
         if constexpr (KV) L<r - 1>::sts(sm + TW, w);
         if constexpr (same_warp_bits<L<r - 1>, L<r>>()) {
@@ -515,6 +539,7 @@ struct PassBody {
         } else {
           __syncthreads();
         }
+        jitter(11 + 2 * r);
         L<r>::lds(sm, v);
         if constexpr (KV) L<r>::lds(sm + TW, w);
       }

@@ -213,6 +213,7 @@ extern "C" {
 
 int b200_bitonic_release_scratch(void) {
   drop_graphs();
+  release_multi_ctx();
   {
     std::lock_guard<std::mutex> lk(g_pipe_mu);
     for (HostPipe* hp : g_pipes) {

@@ -6,8 +6,8 @@
 
 namespace b200 {
 
-constexpr int kMergeThreads = 256;
-constexpr int kMergeItems = 8;
-constexpr uint64_t kMergeTile = (uint64_t)kMergeThreads * kMergeItems;
+// merge_bitonic_kernel: one 2^kMergeC-key bitonic tile per CTA
+constexpr int kMergeC = 13;
+constexpr uint64_t kMergeTile = uint64_t{1} << kMergeC;
 
 }  // namespace b200

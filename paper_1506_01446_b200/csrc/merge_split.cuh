@@ -10,10 +10,10 @@
 //
 // Both operations are "output window [o_begin, o_begin + o_len) of
 // merge(A[0..la), B[0..lb))".  merge_partition_kernel finds, for every
-// 2048-key output tile, how many keys come from A (binary search on the
-// diagonal of the virtual merge, A first on ties); merge_tile_kernel stages
-// the two input windows in shared memory, each thread finds its own 8-key
-// sub-diagonal, merges serially and the CTA writes the tile back coalesced.
+// 8192-key output tile, how many keys come from A (binary search on the
+// diagonal of the virtual merge, A first on ties); merge_bitonic_kernel
+// stages the tile's two input windows (B reversed) in shared memory and
+// sorts the resulting bitonic sequence with the last phase of the network.
 // A or B may be a peer-device pointer: each CTA then reads only the part of
 // the partner shard that lands in its output tile, over NVLink, inside the
 // kernel (the exchange is fused into the merge and moves ~m/2 keys).
@@ -21,6 +21,7 @@
 
 #include <cstdint>
 
+#include "bitonic_static.cuh"
 #include "merge_consts.hpp"
 
 namespace b200 {
@@ -40,6 +41,10 @@ __device__ __forceinline__ uint64_t corank_global(uint64_t d, const uint32_t* A,
   return lo;
 }
 
+// One thread per output-tile boundary: binary search on the diagonal.  (A
+// 33-ary warp search -- 32 lanes probing at once -- cut the dependent loads
+// from 29 to 6 at 2^29 keys but read ~8x more DRAM sectors; measured
+// slower on B200 at every size from 2^24 up.)
 __global__ void merge_partition_kernel(const uint32_t* __restrict__ A, uint64_t la,
                                        const uint32_t* __restrict__ B, uint64_t lb,
                                        uint64_t o_begin, uint64_t o_len, uint32_t kx,
@@ -51,49 +56,116 @@ __global__ void merge_partition_kernel(const uint32_t* __restrict__ A, uint64_t 
   coranks[t] = corank_global(o_begin + d, A, la, B, lb, kx);
 }
 
-__global__ void __launch_bounds__(kMergeThreads)
-merge_tile_kernel(const uint32_t* __restrict__ A, uint64_t la,
-                  const uint32_t* __restrict__ B, uint64_t lb, uint64_t o_begin,
-                  uint64_t o_len, uint32_t kx, const uint64_t* __restrict__ coranks,
-                  uint32_t* __restrict__ out) {
-  __shared__ uint32_t s_in[kMergeTile];
-  __shared__ uint32_t s_out[kMergeTile];
+// One output tile per CTA, merged as a bitonic sequence: the tile's A window
+// (ascending) followed by its B window reversed is a bitonic sequence of
+// kMergeTile = 2^kMergeC keys for ANY split na + nb, so the last phase of
+// the network -- steps on local bits kMergeC-1..0, all ascending -- sorts
+// it.  That phase runs on the round engine of the sort passes
+// (bitonic_static.cuh: registers + conflict-free padded shared memory), so
+// the merge has no data-dependent shared-memory traffic (the serial
+// per-thread merge it replaced was bank-conflict bound: 2.3-2.6 TB/s on a
+// 2^29-key merge-split).  A partial last tile is padded with the order's
+// maximum between the two runs (keeping it bitonic); the padding sorts to
+// the end and is not stored.
+template <int C = kMergeC, int R = 5>
+__global__ void __launch_bounds__(threads_for<C, R>(), 3)  // 85 registers: 32 loads in flight
+merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
+                     uint64_t o_begin, uint64_t o_len, uint32_t kx,
+                     const uint64_t* __restrict__ coranks, uint32_t* __restrict__ out,
+                     uint32_t one, uint32_t mone) {
+  using Body = PassBody<C, 1, C - 1, -1, R, 0>;
+  constexpr int T = threads_for<C, R>();
+  constexpr int N = 1 << C;
+  extern __shared__ uint32_t smem[];
   const uint64_t c = blockIdx.x;
-  const uint64_t o0 = c * kMergeTile;
-  const uint64_t o1 = (o0 + kMergeTile < o_len) ? o0 + kMergeTile : o_len;
-  const uint64_t d0 = o_begin + o0, d1 = o_begin + o1;
+  const uint64_t o0 = c * (uint64_t)N;
+  const uint64_t o1 = (o0 + N < o_len) ? o0 + N : o_len;
   const uint64_t i0 = coranks[c], i1 = coranks[c + 1];
-  const uint64_t j0 = d0 - i0, j1 = d1 - i1;
-  const int na = (int)(i1 - i0), nbk = (int)(j1 - j0), L = na + nbk;
-
-  for (int x = threadIdx.x; x < na; x += kMergeThreads) s_in[x] = A[i0 + x] ^ kx;
-  for (int x = threadIdx.x; x < nbk; x += kMergeThreads) s_in[na + x] = B[j0 + x] ^ kx;
-  __syncthreads();
-
-  const uint32_t* sA = s_in;
-  const uint32_t* sB = s_in + na;
-  int dt = threadIdx.x * kMergeItems;
-  if (dt > L) dt = L;
-  int lo = dt > nbk ? dt - nbk : 0;
-  int hi = dt < na ? dt : na;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (sA[mid] <= sB[dt - mid - 1]) lo = mid + 1;
-    else hi = mid;
-  }
-  int i = lo, j = dt - lo;
+  const uint64_t j1 = o_begin + o1 - i1;
+  const int na = (int)(i1 - i0);
+  const int L = (int)(o1 - o0);
+  // stage: local j -> A[i0 + j] (j < na, ascending), padding (the maximum),
+  // B backwards in the last nb slots (descending): ascending, flat,
+  // descending is bitonic.  All of a thread's loads are issued before the
+  // first store (memory-level parallelism).
+  {
+    // 16-byte loads on the aligned interior of both windows (the edges, at
+    // most 3 + 3 keys per window, and the padding are stored separately).
+    // Chunk u of the concatenated chunk list is A chunk u or B chunk u-nA4;
+    // each thread issues all its chunk loads before any store.
+    const int nbk = L - na;
+    const uint64_t j0 = j1 - (uint64_t)nbk;
+    const uint64_t a0 = (i0 + 3) & ~uint64_t{3}, a1e = i1 & ~uint64_t{3};
+    const uint64_t b0 = (j0 + 3) & ~uint64_t{3}, b1e = j1 & ~uint64_t{3};
+    const bool va = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && a1e > a0 && a0 <= i1;
+    const bool vb = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && b1e > b0 && b0 <= j1;
+    const int nA4 = va ? (int)((a1e - a0) >> 2) : 0;
+    const int nB4 = vb ? (int)((b1e - b0) >> 2) : 0;
+    constexpr int Q = N / 4 / T;  // chunk slots per thread
+    uint4 x[Q];
 #pragma unroll
-  for (int q = 0; q < kMergeItems; ++q) {
-    const int o = dt + q;
-    if (o < L) {
-      const bool takeA = (j >= nbk) || (i < na && sA[i] <= sB[j]);
-      s_out[o] = takeA ? sA[i] : sB[j];
-      i += takeA ? 1 : 0;
-      j += takeA ? 0 : 1;
+    for (int q = 0; q < Q; ++q) {
+      const int u = threadIdx.x + q * T;
+      const uint4* src = u < nA4 ? reinterpret_cast<const uint4*>(A + a0) + u
+                                 : reinterpret_cast<const uint4*>(B + b0) + (u - nA4);
+      if (u < nA4 + nB4) x[q] = __ldg(src);
     }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int u = threadIdx.x + q * T;
+      if (u < nA4) {
+        const uint32_t j = (uint32_t)(a0 - i0) + 4u * (uint32_t)u;  // A slot
+        smem[smem_pad(j)] = x[q].x ^ kx;
+        smem[smem_pad(j + 1)] = x[q].y ^ kx;
+        smem[smem_pad(j + 2)] = x[q].z ^ kx;
+        smem[smem_pad(j + 3)] = x[q].w ^ kx;
+      } else if (u < nA4 + nB4) {
+        // B[g] -> slot N - 1 - (g - j0)
+        const uint32_t j = (uint32_t)(N - 1) - (uint32_t)(b0 - j0) - 4u * (uint32_t)(u - nA4);
+        smem[smem_pad(j)] = x[q].x ^ kx;
+        smem[smem_pad(j - 1)] = x[q].y ^ kx;
+        smem[smem_pad(j - 2)] = x[q].z ^ kx;
+        smem[smem_pad(j - 3)] = x[q].w ^ kx;
+      }
+    }
+    // edges (keys outside the 16-byte interiors) and padding
+    const uint64_t ea0 = va ? a0 : i1, ea1 = va ? a1e : i1;  // A interior [ea0, ea1)
+    const uint64_t eb0 = vb ? b0 : j1, eb1 = vb ? b1e : j1;
+    for (uint64_t g = i0 + threadIdx.x; g < ea0; g += T) smem[smem_pad((uint32_t)(g - i0))] = A[g] ^ kx;
+    for (uint64_t g = ea1 + threadIdx.x; g < i1; g += T) smem[smem_pad((uint32_t)(g - i0))] = A[g] ^ kx;
+    for (uint64_t g = j0 + threadIdx.x; g < eb0; g += T)
+      smem[smem_pad((uint32_t)(N - 1) - (uint32_t)(g - j0))] = B[g] ^ kx;
+    for (uint64_t g = eb1 + threadIdx.x; g < j1; g += T)
+      smem[smem_pad((uint32_t)(N - 1) - (uint32_t)(g - j0))] = B[g] ^ kx;
+    for (int j = na + threadIdx.x; j < N - nbk; j += T) smem[smem_pad((uint32_t)j)] = 0xFFFFFFFFu;
   }
   __syncthreads();
-  for (int x = threadIdx.x; x < L; x += kMergeThreads) out[o0 + x] = s_out[x] ^ kx;
+  typename Body::Ctx cx;
+  cx.keys = out;
+  cx.vals = nullptr;
+  cx.gbase = o0;
+  cx.y = C;
+  cx.uA = cx.uB = cx.uC = 0u;  // one ascending phase, no direction bit
+  cx.gin = cx.gout = cx.gin_lo = cx.gout_lo = 0u;
+  cx.fs = FmaSplit{one, mone};
+  uint32_t v[1 << R];
+  uint32_t w[1 << R];
+  Body::template L<0>::lds(smem, v);
+  Body::template rounds<0>(cx, smem, v, w);
+  using LL = typename Body::template L<Body::NRND - 1>;
+  LL::sts(smem, v);
+  __syncthreads();
+  uint32_t* o = out + o0;
+  if (L == N && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+#pragma unroll 4
+    for (int q = threadIdx.x; q < N / 4; q += T) {
+      const uint32_t p = smem_pad(4u * q);
+      reinterpret_cast<uint4*>(o)[q] =
+          make_uint4(smem[p] ^ kx, smem[p + 1] ^ kx, smem[p + 2] ^ kx, smem[p + 3] ^ kx);
+    }
+  } else {
+    for (int j = threadIdx.x; j < L; j += T) o[j] = smem[smem_pad((uint32_t)j)] ^ kx;
+  }
 }
 
 }  // namespace b200

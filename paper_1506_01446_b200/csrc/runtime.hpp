@@ -138,6 +138,9 @@ int run_graphed(const GraphKey& key, cudaStream_t s, Fn&& fn) {
   return B200_OK;
 }
 
+// ---- multi-GPU context (multi.cu): cached streams / scratch of sort_u32_multi
+void release_multi_ctx();
+
 // ---- the sort and the merge path
 // Validates and runs the whole plan (or only pass `only`, when >= 0).
 // key_xor: 0x80000000 for int32 keys (for 64-bit keys: applied to the hi

@@ -27,8 +27,10 @@ becomes a merge-split (block 0-1 principle):
    reads the partner's shard straight out of the partner GPU's memory over
    NVLink/NVSwitch -- only the part of it that lands in this rank's output
    window, ~m/2 keys on random data -- while it writes the merged output
-   locally.  Two host barriers per step order the steps (partner's shard
-   final before the read; read done before the buffer is reused).
+   locally.  The steps are ordered on the device with interprocess CUDA
+   events (partner's shard final before the read; read done before the
+   buffer is reused); one host-only barrier per step orders the event
+   records before the waits, without draining the GPUs.
 
 Afterwards rank r holds global sorted positions [r*m, (r+1)*m).
 
@@ -137,12 +139,56 @@ class PeerShards:
                 self.ptrs.append(row)
         except Exception as e:  # e.g. no peer access / IPC not permitted here
             err = repr(e)
+        # interprocess events, one per network step boundary (E[0..S]):
+        # E_r[s] is recorded by rank r once its shard for step s is final
+        nev = len(network_steps(world)) + 1
+        self.events = []   # events[r][s], rank r's events opened here
+        self._own_events, self._opened_events = [], []
+        ev_handles = []
+        if err is None:
+            try:
+                for _ in range(nev):
+                    ev, h = ctypes.c_void_p(), _native.IpcHandle()
+                    _check(self._lib.b200_bitonic_ipc_event_create(ctypes.byref(ev),
+                                                                   ctypes.byref(h)))
+                    self._own_events.append(ev.value)
+                    ev_handles.append(bytes(h.bytes))
+            except Exception as e:
+                err = repr(e)
+        everyone_ev = [None] * world
+        dist.all_gather_object(everyone_ev, ev_handles, group=group)
+        if err is None:
+            try:
+                for r in range(world):
+                    if r == rank:
+                        self.events.append(list(self._own_events))
+                        continue
+                    row = []
+                    for hb in everyone_ev[r]:
+                        ev, h = ctypes.c_void_p(), _native.IpcHandle()
+                        ctypes.memmove(h.bytes, hb, len(hb))
+                        _check(self._lib.b200_bitonic_ipc_event_open(ctypes.byref(h),
+                                                                     ctypes.byref(ev)))
+                        row.append(ev.value)
+                        self._opened_events.append(ev.value)
+                    self.events.append(row)
+            except Exception as e:
+                err = repr(e)
         # collective verdict: every rank mapped every peer, or nobody uses them
         oks = [None] * world
         dist.all_gather_object(oks, err is None, group=group)
         if not all(oks):
             self.close()
             raise PeerUnavailable(err or "a peer rank could not map the IPC buffers")
+        # host-only barrier (orders event records before the partners' waits
+        # without draining any GPU stream): the group itself when it is gloo,
+        # else a gloo group over the same ranks
+        backend = dist.get_backend(group)
+        if backend == "gloo":
+            self.host_group = group
+        else:
+            members = dist.get_process_group_ranks(group) if group is not None else None
+            self.host_group = dist.new_group(ranks=members, backend="gloo")
 
     def close(self) -> None:
         import ctypes
@@ -150,7 +196,10 @@ class PeerShards:
             self._lib.b200_bitonic_ipc_close(ctypes.c_void_p(p))
         for p in self.local:
             self._lib.b200_bitonic_ipc_free(ctypes.c_void_p(p))
+        for e in getattr(self, "_opened_events", []) + getattr(self, "_own_events", []):
+            self._lib.b200_bitonic_event_destroy(ctypes.c_void_p(e))
         self._opened, self.local = [], []
+        self._opened_events, self._own_events = [], []
 
 
 _PEER_CACHE: dict = {}
@@ -178,38 +227,64 @@ def _peer_shards(m, itemsize, group, rank, world, device):
 
 def _peer_partitioned_sort(shard, descending, group, rank, world, stats):
     """Local sort, then every merge-split step as one kernel reading the
-    partner's shard through CUDA IPC peer memory."""
+    partner's shard through CUDA IPC peer memory.  Steps are ordered on the
+    device: rank r records its interprocess event E_r[s] when its shard for
+    step s is final; before step s its stream waits on the partner's E[s]
+    (the partner's shard is final) and on the previous partner's E[s] (that
+    rank has finished reading the buffer this step overwrites).  One
+    host-only (gloo) barrier per step orders every record before the waits
+    on it; the GPUs never drain between steps."""
     import ctypes
     from . import _native, _check, _stream_ptr
     lib = _native.lib()
     m = shard.numel()
     kx = key_xor_for(shard.dtype, descending)
+    steps = network_steps(world)
     with torch.cuda.device(shard.device):
         stream = torch.cuda.current_stream(shard.device)
         sp = ctypes.c_void_p(_stream_ptr(stream))
         bufs = _peer_shards(m, shard.element_size(), group, rank, world, shard.device)
+        ev = bufs.events
+        counts = torch.zeros(len(steps), dtype=torch.int64, device=shard.device)
         cur = 0
         _check(lib.b200_bitonic_copy(ctypes.c_void_p(bufs.local[cur]),
                                      ctypes.c_void_p(shard.data_ptr()), bufs.bytes, sp))
         sort_fn = lib.b200_bitonic_sort_i32 if shard.dtype == torch.int32 \
             else lib.b200_bitonic_sort_u32
         _check(sort_fn(ctypes.c_void_p(bufs.local[cur]), m, int(bool(descending)), sp))
-        for q, s in network_steps(world):
+        _check(lib.b200_bitonic_event_record(ctypes.c_void_p(ev[rank][0]), sp))
+        dist.barrier(bufs.host_group)  # every E[0] record is enqueued
+        prev_partner = None
+        for i, (q, s) in enumerate(steps):
             partner, keep_high = step_role(rank, q, s)
-            stream.synchronize()
-            dist.barrier(group)  # every rank's current shard is final
-            _check(lib.b200_bitonic_merge_split_u32(
+            _check(lib.b200_bitonic_stream_wait_event(sp, ctypes.c_void_p(ev[partner][i])))
+            if prev_partner is not None and prev_partner != partner:
+                _check(lib.b200_bitonic_stream_wait_event(
+                    sp, ctypes.c_void_p(ev[prev_partner][i])))
+            _check(lib.b200_bitonic_merge_split_u32_count(
                 ctypes.c_void_p(bufs.local[cur]), ctypes.c_void_p(bufs.ptrs[partner][cur]),
                 m, int(keep_high), ctypes.c_uint32(kx & 0xFFFFFFFF),
-                ctypes.c_void_p(bufs.local[cur ^ 1]), sp))
-            stream.synchronize()
-            dist.barrier(group)  # the partner has finished reading our shard
+                ctypes.c_void_p(bufs.local[cur ^ 1]), sp,
+                ctypes.c_void_p(counts.data_ptr() + 8 * i)))
+            _check(lib.b200_bitonic_event_record(ctypes.c_void_p(ev[rank][i + 1]), sp))
+            dist.barrier(bufs.host_group)  # every E[i+1] record is enqueued
+            prev_partner = partner
             cur ^= 1
+        # every rank has finished its last read of our buffers before the
+        # result leaves them (and before a later call refills them)
+        for r in range(world):
+            if r != rank:
+                _check(lib.b200_bitonic_stream_wait_event(
+                    sp, ctypes.c_void_p(ev[r][len(steps)])))
         _check(lib.b200_bitonic_copy(ctypes.c_void_p(shard.data_ptr()),
                                      ctypes.c_void_p(bufs.local[cur]), bufs.bytes, sp))
     if stats is not None:
         stats["exchange"] = "peer"
-        stats["steps"] = len(network_steps(world))
+        stats["steps"] = len(steps)
+        stats["ordering"] = "interprocess CUDA events (device-side); gloo host barrier per step"
+        # keys this rank read from its partner per step (device tensor; x4 = bytes
+        # over NVLink); materialise with partner_keys.tolist() after timing
+        stats["partner_keys"] = counts
     return shard
 
 

@@ -1,4 +1,10 @@
-"""Workload for compute-sanitizer (racecheck / synccheck / memcheck / initcheck).
+"""Race-check workload: every kernel family once, checked against numpy.
+
+Run against the jitter build (tests/test_gpu_jitter.py sets
+B200_BITONIC_LIB=paper_1506_01446_b200/libb200_bitonic_jitter.so, built with
+-DB200_JITTER: random sleeps at every shared-memory hand-off), and meant for
+compute-sanitizer (racecheck / synccheck / memcheck) where that tool is
+allowed -- on this pool it is not (runs are refused, exit 86).
 
 Runs every kernel family of the library once at small sizes -- the tile sort,
 the merge passes (13/14-bit cosets and the 16-key variants), the batched
@@ -6,7 +12,8 @@ tiles, key-value and 64-bit kernels, the merge-path kernels (merge_tile /
 merge_partition) and the pipelined host entry -- and checks each result
 against numpy.  Usage (on the GPU box):
 
-    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+    B200_BITONIC_LIB=.../libb200_bitonic_jitter.so python tests/race_workload.py
+    compute-sanitizer --tool racecheck python tests/race_workload.py
 
 Exit code 0 = all results correct; the sanitizer's own summary line reports
 hazards / errors.
@@ -120,5 +127,5 @@ for _ in range(2):
     b.sort_host(h)
     check("host entry 2^18 x4 chunks", h.copy(), np.sort(x))
 
-print("sanitize_run:", "OK" if not bad else f"FAILED {bad}")
+print("race_workload:", "OK" if not bad else f"FAILED {bad}")
 sys.exit(1 if bad else 0)
