@@ -22,7 +22,7 @@ SOURCES = [os.path.join(CSRC, f) for f in
            ["bitonic_sort.cu", "k_tile.cu", "k_merge11.cu", "k_merge12.cu",
             "k_merge13.cu", "k_merge14.cu", "k_merge15.cu", "k_merge12r4.cu",
             "k_merge13r4.cu", "k_merge14r4.cu", "k_merge12kv.cu", "k_merge13kv.cu",
-            "k_merge12k64.cu", "k_merge13k64.cu", "k_tile_k64.cu", "k_cluster.cu", "k_tile_tma.cu",
+            "k_merge12k64.cu", "k_merge13k64.cu", "k_tile_k64.cu", "k_cluster.cu", "k_tile_tma.cu", "k_virt.cu",
             "host_entry.cu", "multi.cu"]]
 HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
            if f.endswith((".cuh", ".hpp", ".h"))]

@@ -134,9 +134,10 @@ struct ClusterPass {
     pdl_wait();
     B1::load(c1, sm, v, w);
     B1::template rounds<0>(c1, sm, v, w);
+    B1::tail(c1, v, w);
     // leave phase A's domain, enter phase B's (both CTA-uniform; phase B's is
     // the same in both CTAs, so the peer's keys arrive in the right domain)
-    using LL = typename B1::template L<B1::NRND - 1>;
+    using LL = typename B1::template L<B1::NRE - 1>;
     const uint32_t m = c1.uA ^ c2.uB;
 #pragma unroll
     for (int e = 0; e < NR; ++e) v[e] ^= m;
@@ -151,6 +152,7 @@ struct ClusterPass {
     cluster_wait();    // the peer has read ours: shared memory may be reused
     jitter(7);
     B2::template rounds<1>(c2, sm, v, w);
+    B2::tail(c2, v, w);
     B2::store(c2, sm, v, w);
     pdl_trigger();
   }

@@ -85,6 +85,11 @@ struct PassParams {
   // 1 and 0xFFFFFFFF, opaque to the compiler: operands of the IMAD form of
   // max() that moves part of the compare-exchange work to the FMA pipe
   uint32_t one, mone;
+  // Virtual padding (non-power-of-two lengths, *_VIRT kernels): keys at
+  // indices >= nreal are virtual; phase p's direction bit is bit p of
+  // (index ^ dxor), dxor = nreal - 1.  Ignored by the other kernels.
+  uint64_t nreal;
+  uint64_t dxor;
   // 1: CTAs take their cosets in reverse order.  Consecutive passes run in
   // opposite directions, so a pass starts on the cosets the previous pass
   // wrote last -- still in L2 when the array is larger than L2.

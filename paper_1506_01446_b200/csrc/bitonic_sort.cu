@@ -63,6 +63,7 @@ b200::PlanOptions plan_options() {
   if (const char* e = std::getenv("B200_BITONIC_CLUSTER_COST")) o.cluster_cost = std::atof(e);
   if (const char* e = std::getenv("B200_BITONIC_MID_LRUN")) o.mid_lrun = std::atoi(e);
   if (const char* e = std::getenv("B200_BITONIC_R14")) o.regbits14 = std::atoi(e);
+  if (const char* e = std::getenv("B200_BITONIC_TILE_C")) o.tile_c = std::atoi(e);
   return o;
 }
 
@@ -160,6 +161,10 @@ std::atomic<int> g_pdl{1};  // programmatic dependent launch between passes
 // 32 keys per thread.
 // mode: 0 keys, 1 key + payload, 2 64-bit keys (two word arrays).
 b200::PassFn select_kernel(const b200::PlanPass& q, int* R_out, int mode) {
+  if (mode == 3) {  // virtual padding (keys only)
+    *R_out = 5;
+    return b200::find_virtual_kernel(q.tile_sort != 0, q.C, q.segA_hi, q.segB_lo, q.R);
+  }
   if (q.cluster) {
     *R_out = 5;
     return mode == 0 ? b200::find_cluster_kernel(q.segA_hi, 5) : nullptr;
@@ -248,6 +253,7 @@ cudaError_t launch_tile_tma(const b200::PlanPass& q, b200::PassParams p, uint64_
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
+// mode: 0 keys, 1 key + payload, 2 64-bit keys, 3 keys with virtual padding
 cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p, cudaStream_t s,
                         int mode) {
   if (q.tile_sort && mode == 0 && q.R == 5 && q.p_end == q.C && tma_enabled() &&
@@ -257,7 +263,7 @@ cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p, cudaStream_
     if (done || e != cudaSuccess) return e;
   }
   int R = 5;
-  const bool kv = mode != 0;
+  const bool kv = mode == 1 || mode == 2;
   b200::PassFn f = select_kernel(q, &R, mode);
   if (f == nullptr) return cudaErrorNotSupported;  // no such key-value shape
   const void* fn = reinterpret_cast<const void*>(f);
@@ -292,7 +298,7 @@ struct PlanKey {
   double wide_tail_cost;
   bool cluster;
   double cluster_cost;
-  int mid_lrun, regbits14;
+  int mid_lrun, regbits14, tile_c;
   bool operator==(const PlanKey& o) const {
     return k == o.k && batch == o.batch && cmax == o.cmax && cmin == o.cmin &&
            lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp &&
@@ -300,7 +306,7 @@ struct PlanKey {
            trip_cost == o.trip_cost && mixed_c == o.mixed_c &&
            wide_tail_cost == o.wide_tail_cost && cluster == o.cluster &&
            cluster_cost == o.cluster_cost && mid_lrun == o.mid_lrun &&
-           regbits14 == o.regbits14;
+           regbits14 == o.regbits14 && tile_c == o.tile_c;
   }
 };
 std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
@@ -308,7 +314,7 @@ std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
   const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.tile_regbits,
                     o.cmerge, o.dp, o.kv, o.trip_cost, o.mixed_c, o.wide_tail_cost,
-                    o.cluster, o.cluster_cost, o.mid_lrun, o.regbits14};
+                    o.cluster, o.cluster_cost, o.mid_lrun, o.regbits14, o.tile_c};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;
@@ -365,6 +371,7 @@ GraphKey make_key(int kind, const void* p0, const void* p1, uint64_t n, uint64_t
   key.cluster = o.cluster;
   key.mid_lrun = o.mid_lrun;
   key.regbits14 = o.regbits14;
+  key.tile_c = o.tile_c;
   key.cluster_cost = o.cluster_cost;
   key.dp = o.dp;
   key.generic = g_force_generic.load();
@@ -392,8 +399,13 @@ void drop_graphs() {
 // word).  d_vals: payloads (mode 1) or the lo words of 64-bit keys whose hi
 // words are d_keys (mode 2).
 int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
-              uint32_t key_xor, cudaStream_t stream, int only, uint32_t* d_vals, int mode) {
+              uint32_t key_xor, cudaStream_t stream, int only, uint32_t* d_vals, int mode,
+              uint64_t nreal) {
   if (mode < 0) mode = d_vals != nullptr ? 1 : 0;
+  const bool virt = nreal != 0 && nreal < n_per;
+  if (virt && (batch != 1 || d_vals != nullptr || mode != 0)) {
+    return fail(B200_CONFIG, "virtual padding: single key-only arrays");
+  }
   if (mode != 0 && d_vals == nullptr) return fail(B200_CONFIG, "null second array");
   if (n_per < 2 || !is_pow2(n_per)) {
     return fail(B200_INVALID_SIZE,
@@ -412,6 +424,10 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
   std::vector<b200::PlanPass> plan;
   b200::PlanOptions popt = plan_options();
   popt.kv = d_vals != nullptr;
+  if (virt) {
+    popt = b200::PlanOptions{};  // the virtual kernels' fixed shapes (no tuning knobs)
+    popt.virt = true;
+  }
   try {
     plan = cached_plan(k, batch, popt);
   } catch (const std::exception& e) {
@@ -447,7 +463,9 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
       p.one = 1u;
       p.mone = 0xFFFFFFFFu;
       p.reverse = (reverse_enabled() && (i & 1) && !q.cluster) ? 1 : 0;
-      cudaError_t e = launch_pass(q, p, st, mode);
+      p.nreal = virt ? nreal : ~uint64_t{0};
+      p.dxor = virt ? nreal - 1 : 0;
+      cudaError_t e = launch_pass(q, p, st, virt ? 3 : mode);
       if (e == cudaErrorNotSupported) {
         return fail(B200_CONFIG,
                     "no key-value kernel for this tile size (use tile_bits 0, 12 or 13)");
@@ -457,9 +475,9 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
     return B200_OK;
   };
   if (only >= 0 || plan.size() < 2) return launch_all(stream);
-  return run_graphed(make_key(0, d_keys, d_vals, n_per, batch, descending, key_xor, mode, 0,
-                              popt),
-                     stream, launch_all);
+  GraphKey gk = make_key(0, d_keys, d_vals, n_per, batch, descending, key_xor, mode, 0, popt);
+  gk.nreal = virt ? nreal : 0;
+  return run_graphed(gk, stream, launch_all);
 }
 
 // ---- merge path ----------------------------------------------------------------
@@ -560,6 +578,11 @@ __global__ void pad_fill_kernel(uint32_t* dst, const uint32_t* src, uint64_t n,
   }
 }
 
+bool virtual_padding_disabled() {
+  const char* e = std::getenv("B200_BITONIC_VIRTUAL");
+  return e && std::strcmp(e, "0") == 0;
+}
+
 int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
                 cudaStream_t s) {
   if (n < 1) return fail(B200_INVALID_SIZE, "length must be >= 1");
@@ -597,6 +620,12 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
     cudaFreeAsync(cor, s);
     cudaFreeAsync(out, s);
     return rc;
+  }
+  if (aligned && m >= (uint64_t{1} << 15) && !virtual_padding_disabled()) {
+    // Virtual padding: the 2^j-key network runs in place on the n real keys;
+    // the m - n virtual keys are never loaded or stored (bitonic_static.cuh,
+    // VIRT kernels) -- no scratch copy, no copy back.
+    return sort_impl(d_keys, m, 1, descending, key_xor, s, -1, nullptr, 0, n);
   }
   // padding = the largest key in the sort's order (sorts last, discarded)
   const uint32_t gmask = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);

@@ -192,6 +192,43 @@ __device__ __forceinline__ void stage_out(const uint32_t* sm, uint32_t* keys,
   }
 }
 
+// ---- virtual padding (non-power-of-two lengths, no copy) -----------------------
+// The array holds nreal keys; indices nreal .. 2^k - 1 are virtual.  A
+// virtual key never reaches memory: loads give the phase domain's maximum
+// (0xFFFFFFFF), stores skip it.  With the direction rule of the virtual plans
+// (phase p's block is descending iff bit p of (index ^ (nreal - 1)) is set)
+// the block holding index nreal - 1 is ascending at every level, so in the
+// phase domain every compare-exchange that pairs a real key with a virtual
+// one keeps the real key in place (the virtual index is the higher one) --
+// the reference's pad_to_pow2 + sort + truncate (bench.cpp:366-377) without
+// the padded copy.  Only CTAs whose coset straddles nreal take these paths.
+template <int C, int A, int DBIT, int R>
+__device__ __forceinline__ void stage_in_virtual(uint32_t* sm, const uint32_t* keys,
+                                                 uint64_t gbase, int y, uint32_t m_uniform,
+                                                 uint64_t nreal) {
+  using TL = Tile<C>;
+  constexpr int T = 1 << (C - R), N = TL::N;
+  for (uint32_t j = threadIdx.x; j < (uint32_t)N; j += T) {
+    uint32_t m = m_uniform;
+    if constexpr (DBIT >= 0) m ^= 0u - ((j >> DBIT) & 1u);
+    const uint64_t g = gbase + Coset<C, A>::goff(j, y);
+    sm[TL::pad(j)] = g < nreal ? (keys[g] ^ m) : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+}
+
+template <int C, int A, int R>
+__device__ __forceinline__ void stage_out_virtual(const uint32_t* sm, uint32_t* keys,
+                                                  uint64_t gbase, int y, uint64_t nreal) {
+  using TL = Tile<C>;
+  constexpr int T = 1 << (C - R), N = TL::N;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < (uint32_t)N; j += T) {
+    const uint64_t g = gbase + Coset<C, A>::goff(j, y);
+    if (g < nreal) keys[g] = sm[TL::pad(j)];
+  }
+}
+
 template <int C, int R>
 constexpr int threads_for() {
   return 1 << (C - R);
@@ -216,9 +253,48 @@ constexpr int min_blocks_for() {
 // MODE 0: keys only.  MODE 1: key + 32-bit payload (the payload array
 // follows its key).  MODE 2: 64-bit keys split into a hi-word array (v) and
 // a lo-word array (w), compared lexicographically.
+// ---- shuffle tail ---------------------------------------------------------------
+// When the steps of a pass's LAST round all touch lane bits of the round
+// before it, those steps run as warp shuffles (SHFL.BFLY + one min/max per
+// key) in that layout and the final shared-memory round trip (STS + barrier
+// + LDS of every key) disappears.  B200_SHFL_TAIL = the most steps done this
+// way (0 = off).  E.g. the 2^13-key tile sort's 17th round is the single
+// step on bit 0 -- a lane bit of round 16's layout.
+// Measured on B200 (tools/perf_probe.py, tools/pass_times.py, A/B against
+// -DB200_SHFL_TAIL=0): no gain at any size -- 2^16 22.3/22.5 us, 2^20 49.1
+// both, 2^24 479/475 us, 2^28 11.06/10.99 ms, batched 102-105 us both --
+// and the 2^28 sort's last pass lost its direct store (366 vs 315 us); the
+// tile sort saves one of 18 round trips but is ALU-bound.  Off by default.
+#ifndef B200_SHFL_TAIL
+#define B200_SHFL_TAIL 0
+#endif
+
+template <class LP>
+constexpr int lane_of(int b) {
+  const int lanes = LP::NT < 5 ? LP::NT : 5;
+  for (int i = 0; i < lanes; ++i)
+    if (LP::tpos(i) == b) return i;
+  return -1;
+}
+
+template <class S, class RD, class LP, int NRND, int KIND, int R>
+constexpr bool shfl_tail_ok() {
+  if (B200_SHFL_TAIL <= 0 || NRND < 2 || LP::NT < 5) return false;
+  const int b0 = RD::begin(NRND - 1), e = S::len();
+  if (e - b0 > B200_SHFL_TAIL) return false;
+  for (int i = b0; i < e; ++i) {
+    if (lane_of<LP>(S::bit(i)) < 0) return false;
+    if (KIND == 0 && S::phase(i) < R) return false;  // natural-domain phases
+    if (S::phase(i) != S::phase(b0)) return false;
+  }
+  return true;
+}
+
 // AO >= 0 overrides the coset's low-run length A (the cluster passes run a
 // tail on a 2^C sub-coset whose low run is shorter than C).
-template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), int MODE = 0, int AO = -1>
+// VIRT: the virtual-padding variant (non-power-of-two single arrays).
+template <int C, int KIND, int SA, int SB, int RR = reg_bits(C), int MODE = 0, int AO = -1,
+          bool VIRT = false>
 struct PassBody {
   static constexpr bool KV = MODE != 0;   // two register arrays
   // FMA-pipe share of the compare-exchange max (Layout::mm)
@@ -247,6 +323,10 @@ struct PassBody {
   static constexpr int NRND = RD::count();
   template <int r>
   using L = Layout<C, RD::mask(r)>;
+  // keys only: the last round may run as shuffles in the previous layout
+  static constexpr bool SHT =
+      MODE == 0 && !VIRT && shfl_tail_ok<S, RD, Layout<C, RD::mask(NRND >= 2 ? NRND - 2 : 0)>, NRND, KIND, R>();
+  static constexpr int NRE = SHT ? NRND - 1 : NRND;  // rounds through shared memory
 
   // local direction bit of phase id ph (-1: uniform / none)
   static constexpr int dloc(int ph) {
@@ -255,7 +335,9 @@ struct PassBody {
     return -1;
   }
   // is phase id ph in the natural domain (tile sort phases < R)
-  static constexpr bool natural(int ph) { return KIND == 0 && ph < R; }
+  // (the virtual variant runs every phase in the phase domain: its
+  // directions carry a runtime flip, see flip())
+  static constexpr bool natural(int ph) { return !VIRT && KIND == 0 && ph < R; }
 
   struct Ctx {
     uint32_t* keys;
@@ -267,7 +349,26 @@ struct PassBody {
     uint32_t gin, gout;   // key-order transforms
     uint32_t gin_lo, gout_lo;  // low-word transforms (MODE 2)
     FmaSplit fs;               // opaque 1 / -1 (FMA-pipe max)
+    // virtual padding (VIRT): real key count, direction flips of the local-
+    // bit phases (bit p of nreal-1), and whether this coset straddles nreal
+    uint64_t nreal;
+    uint32_t xloc, xA;
+    int partial;
   };
+
+  // Runtime direction flip of phase PH when its direction bit is local.
+  template <int PH>
+  __device__ __forceinline__ static uint32_t flip(const Ctx& c) {
+    if constexpr (!VIRT) {
+      return 0u;
+    } else if constexpr (KIND == 0) {
+      if constexpr (PH < C) return 0u - ((c.xloc >> PH) & 1u);
+      else return 0u;
+    } else {
+      if constexpr (PH == 0 && SB >= 0) return c.xA;
+      else return 0u;
+    }
+  }
 
   // uniform mask for phase id ph when its direction bit is not local
   __device__ __forceinline__ static uint32_t uni(const Ctx& c, int ph) {
@@ -303,9 +404,9 @@ struct PassBody {
       if constexpr (lb < 0) {
         return uni(c, PH);
       } else if constexpr (LR::qof(lb) >= 0) {
-        return 0u;
+        return flip<PH>(c);
       } else {
-        return 0u - ((tj >> lb) & 1u);
+        return (0u - ((tj >> lb) & 1u)) ^ flip<PH>(c);
       }
     }
   }
@@ -368,25 +469,6 @@ struct PassBody {
     apply_mask<LR, PH0, PH1, true>(c, v, w, 0u, 0u);
   }
 
-  // Mask of register e, layout LR, phase id ph (0 / ~0).
-  template <class LR, int PH>
-  __device__ __forceinline__ static uint32_t dmask(const Ctx& c, int e, uint32_t tj) {
-    if constexpr (natural(PH)) {
-      return 0u;
-    } else {
-      constexpr int lb = dloc(PH);
-      if constexpr (lb >= 0) {
-        if constexpr (LR::qof(lb) >= 0) {
-          return ((e >> LR::qof(lb)) & 1) ? 0xFFFFFFFFu : 0u;
-        } else {
-          return 0u - ((tj >> lb) & 1u);
-        }
-      } else {
-        return uni(c, PH);
-      }
-    }
-  }
-
   template <class LR, int I>
   __device__ __forceinline__ static void one_step(const Ctx& c, uint32_t (&v)[NR],
                                                   uint32_t (&w)[NR]) {
@@ -409,6 +491,9 @@ struct PassBody {
     if constexpr (I < RD::begin(r + 1)) {
       if constexpr (I > 0 && S::phase(I) != S::phase(I - 1)) {
         transition<L<r>, S::phase(I - 1), S::phase(I)>(c, v, w);
+        if constexpr (VIRT) {
+          if (c.partial) reset_virtual<L<r>>(c, v);
+        }
       }
       one_step<L<r>, I>(c, v, w);
       steps<r, I + 1>(c, v, w);
@@ -421,6 +506,15 @@ struct PassBody {
   template <class LR>
   static constexpr bool direct_ok() {
     return KIND == 1 && LR::lanes_low() && A >= LR::vec_bits() + 5;
+  }
+  // Virtual keys back to the phase domain's maximum (after a transition XOR).
+  template <class LR>
+  __device__ __forceinline__ static void reset_virtual(const Ctx& c, uint32_t (&v)[NR]) {
+    const uint64_t base = c.gbase + Coset<C, A>::goff(LR::thread_j(), c.y);
+    const uint64_t lim = c.nreal > base ? c.nreal - base : 0;  // offsets >= lim are virtual
+#pragma unroll
+    for (int e = 0; e < NR; ++e)
+      if (Coset<C, A>::goff(LR::dep_reg(e), c.y) >= lim) v[e] = 0xFFFFFFFFu;
   }
   template <class LR>
   __device__ __forceinline__ static void gload(const Ctx& c, uint32_t tj, uint32_t (&v)[NR]) {
@@ -483,6 +577,17 @@ struct PassBody {
                                               uint32_t (&w)[NR]) {
     using L0 = L<0>;
     constexpr int PH = S::phase(0);
+    if constexpr (VIRT) {
+      if (c.partial) {  // keys only (the virtual plans are u32 / i32)
+        // a straddling coset always goes through shared memory (scalar,
+        // bounds-checked loads; few registers)
+        constexpr int db = natural(PH) ? -1 : dloc(PH);
+        const uint32_t u = natural(PH) ? 0u : (db >= 0 ? flip<PH>(c) : uni(c, PH));
+        stage_in_virtual<C, A, db, R>(sm, c.keys, c.gbase, c.y, c.gin ^ u, c.nreal);
+        L0::lds(sm, v);
+        return;
+      }
+    }
     if constexpr (direct_ok<L0>()) {
       const uint32_t tj = L0::thread_j();
       gload<L0>(c, tj, v);
@@ -494,7 +599,7 @@ struct PassBody {
       apply_mask<L0, PH, -1, true>(c, v, w, c.gin, c.gin_lo);
     } else {
       constexpr int db = natural(PH) ? -1 : dloc(PH);
-      const uint32_t u = (natural(PH) || db >= 0) ? 0u : uni(c, PH);
+      const uint32_t u = natural(PH) ? 0u : (db >= 0 ? flip<PH>(c) : uni(c, PH));
       stage_in<C, A, db, R>(sm, c.keys, c.gbase, c.y, c.gin ^ u);
       if constexpr (K64) stage_in<C, A, db, R>(sm + TW, c.vals, c.gbase, c.y, c.gin_lo ^ u);
       else if constexpr (KV) stage_in<C, A, -1, R>(sm + TW, c.vals, c.gbase, c.y, 0u);
@@ -503,13 +608,47 @@ struct PassBody {
     }
   }
 
+  // The shuffle tail (SHT): steps I.. on lane bits of layout L<NRE-1>.
+  template <int I>
+  __device__ __forceinline__ static void shfl_steps(const Ctx& c, uint32_t (&v)[NR],
+                                                    uint32_t (&w)[NR]) {
+    if constexpr (I < S::len()) {
+      using LP = L<NRE - 1>;
+      if constexpr (I > 0 && S::phase(I) != S::phase(I - 1)) {
+        transition<LP, S::phase(I - 1), S::phase(I)>(c, v, w);
+      }
+      constexpr int li = lane_of<LP>(S::bit(I));
+      static_assert(li >= 0, "shuffle step on a non-lane bit");
+      const bool upper = (threadIdx.x >> li) & 1u;  // keeps the max (ascending domain)
+#pragma unroll
+      for (int e = 0; e < NR; ++e) {
+        const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, v[e], 1u << li);
+        v[e] = upper ? max(v[e], p) : min(v[e], p);
+      }
+      shfl_steps<I + 1>(c, v, w);
+    }
+  }
+
+  // After the shared-memory rounds: the shuffle tail, if any.  The keys are
+  // then in layout L<NRE - 1>.
+  __device__ __forceinline__ static void tail(const Ctx& c, uint32_t (&v)[NR], uint32_t (&w)[NR]) {
+    if constexpr (SHT) shfl_steps<RD::begin(NRND - 1)>(c, v, w);
+  }
+
   // Registers (last round's layout, last phase's domain) -> keys (+ payloads).
   __device__ __forceinline__ static void store(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR],
                                                uint32_t (&w)[NR]) {
-    using LL = L<NRND - 1>;
+    using LL = L<NRE - 1>;
     constexpr int PH = S::phase(S::len() - 1);
     const uint32_t tj = LL::thread_j();
     apply_mask<LL, PH, -1, true>(c, v, w, c.gout, c.gout_lo);
+    if constexpr (VIRT) {
+      if (c.partial) {
+        LL::sts(sm, v);
+        stage_out_virtual<C, A, R>(sm, c.keys, c.gbase, c.y, c.nreal);
+        return;
+      }
+    }
     if constexpr (direct_ok<LL>()) {
       gstore<LL>(c, tj, v);
       if constexpr (KV) {
@@ -529,7 +668,7 @@ struct PassBody {
   template <int r>
   __device__ __forceinline__ static void rounds(const Ctx& c, uint32_t* sm, uint32_t (&v)[NR],
                                                 uint32_t (&w)[NR]) {
-    if constexpr (r < NRND) {
+    if constexpr (r < NRE) {
       if constexpr (r > 0) {
         jitter(10 + 2 * r);
         L<r - 1>::sts(sm, v);
@@ -554,51 +693,71 @@ struct PassBody {
     pdl_wait();
     load(c, sm, v, w);
     rounds<0>(c, sm, v, w);
+    tail(c, v, w);
     store(c, sm, v, w);
     pdl_trigger();
   }
 };
 
-template <int C, int R = reg_bits(C), int MODE = 0>
+template <int C, int R = reg_bits(C), int MODE = 0, bool VIRT = false>
 __global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R, MODE>())
 tile_sort_kernel(PassParams P) {
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 0, -1, -1, R, MODE>;
+  using B = PassBody<C, 0, -1, -1, R, MODE, -1, VIRT>;
   typename B::Ctx c;
   c.keys = P.keys;
   c.vals = P.vals;
   c.gbase = pass_block(P) << C;
   c.y = C;
   c.uA = c.uB = 0u;
-  c.uC = 0u - dir_bit_global(c.gbase, C, P.kd);
   c.gin = P.gmask_in;
   c.gout = P.gmask_out;
   c.gin_lo = P.gmask_in_lo;
   c.gout_lo = P.gmask_out_lo;
   c.fs = FmaSplit{P.one, P.mone};
+  if constexpr (VIRT) {
+    if (c.gbase >= P.nreal) return;  // every key of this tile is virtual
+    c.nreal = P.nreal;
+    c.partial = c.gbase + ((1u << C) - 1u) >= P.nreal;
+    c.xloc = (uint32_t)(P.dxor & ((1ull << C) - 1ull));
+    c.xA = 0u;
+    c.uC = 0u - dir_bit_global(c.gbase ^ P.dxor, C, P.kd);
+  } else {
+    c.uC = 0u - dir_bit_global(c.gbase, C, P.kd);
+  }
   B::run(c, smem);
 }
 
-template <int C, int SA, int SB, int R = reg_bits(C), int MODE = 0>
+template <int C, int SA, int SB, int R = reg_bits(C), int MODE = 0, bool VIRT = false>
 __global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R, MODE>())
 merge_kernel(PassParams P) {
   static_assert(SA >= 0 || SB >= 0, "empty pass");
   extern __shared__ uint32_t smem[];
-  using B = PassBody<C, 1, SA, SB, R, MODE>;
+  using B = PassBody<C, 1, SA, SB, R, MODE, -1, VIRT>;
   constexpr int A = B::A;
   typename B::Ctx c;
   c.keys = P.keys;
   c.vals = P.vals;
   c.y = P.y;
   c.gbase = Coset<C, A>::base(pass_block(P), P.y);
-  c.uA = 0u - dir_bit_global(c.gbase, P.pA, P.kd);
-  c.uB = 0u - dir_bit_global(c.gbase, P.pB, P.kd);
   c.uC = 0u;
   c.gin = 0u;  // a merge pass never runs first: keys are already transformed
   c.gout = P.gmask_out;
   c.gin_lo = 0u;
   c.gout_lo = P.gmask_out_lo;
   c.fs = FmaSplit{P.one, P.mone};
+  if constexpr (VIRT) {
+    if (c.gbase >= P.nreal) return;  // every key of this coset is virtual
+    c.nreal = P.nreal;
+    c.partial = c.gbase + Coset<C, A>::goff((1u << C) - 1u, P.y) >= P.nreal;
+    c.xloc = 0u;
+    c.xA = 0u - (uint32_t)((P.dxor >> P.pA) & 1u);
+    c.uA = 0u - dir_bit_global(c.gbase ^ P.dxor, P.pA, P.kd);
+    c.uB = 0u - dir_bit_global(c.gbase ^ P.dxor, P.pB, P.kd);
+  } else {
+    c.uA = 0u - dir_bit_global(c.gbase, P.pA, P.kd);
+    c.uB = 0u - dir_bit_global(c.gbase, P.pB, P.kd);
+  }
   B::run(c, smem);
 }
 

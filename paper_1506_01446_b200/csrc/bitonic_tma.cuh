@@ -124,6 +124,7 @@ tile_sort_tma_kernel(PassParams P, const __grid_constant__ CUtensorMap map) {
   }
   __syncthreads();  // the swizzled tile becomes the padded round buffer
   B::template rounds<0>(c, sm, v, w);
+  B::tail(c, v, w);
   B::store(c, sm, v, w);
   pdl_trigger();
 }

@@ -21,6 +21,8 @@ PassFn find_tile_kernel_k64(int C, int R);  // k_tile_k64.cu
 // 2-CTA cluster pass (bitonic_cluster.cuh): tail bits B..0 fused with the
 // head of the next phase on a 2^15-key coset (B in [4, 13]); nullptr otherwise.
 PassFn find_cluster_kernel(int B, int R = 5);
+// Virtual-padding kernels (k_virt.cu): 2^13-key tile / merge shapes, R = 5.
+PassFn find_virtual_kernel(bool tile, int C, int SA, int SB, int R);
 // TMA-loaded tile sort (bitonic_tma.cuh), C in [10, 13], 32 keys per thread
 using TmaTileFn = void (*)(PassParams, const CUtensorMap_st);
 TmaTileFn find_tile_tma_kernel(int C);

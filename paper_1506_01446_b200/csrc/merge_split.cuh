@@ -152,7 +152,8 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
   uint32_t w[1 << R];
   Body::template L<0>::lds(smem, v);
   Body::template rounds<0>(cx, smem, v, w);
-  using LL = typename Body::template L<Body::NRND - 1>;
+  Body::tail(cx, v, w);
+  using LL = typename Body::template L<Body::NRE - 1>;
   LL::sts(smem, v);
   __syncthreads();
   uint32_t* o = out + o0;

@@ -8,26 +8,26 @@
 
 namespace b200 {
 
-template <int C, int A, int R, int MODE>
+template <int C, int A, int R, int MODE, bool VIRT = false>
 PassFn th_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A, R, MODE>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, A - 1, A, R, MODE, VIRT>;
   else return nullptr;
 }
-template <int C, int A, int R, int MODE>
+template <int C, int A, int R, int MODE, bool VIRT = false>
 PassFn ho_entry() {
-  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A, R, MODE>;
+  if constexpr (A >= 2 && A <= C - 1) return &merge_kernel<C, -1, A, R, MODE, VIRT>;
   else return nullptr;
 }
-template <int C, int SA, int R, int MODE>
+template <int C, int SA, int R, int MODE, bool VIRT = false>
 PassFn to_entry() {
-  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1, R, MODE>;
+  if constexpr (SA >= 0 && SA <= C - 1) return &merge_kernel<C, SA, -1, R, MODE, VIRT>;
   else return nullptr;
 }
-template <int C, int R, int MODE, int... I>
+template <int C, int R, int MODE, bool VIRT = false, int... I>
 void fill_merge_table(MergeTable& t, std::integer_sequence<int, I...>) {
-  ((t.th[I] = th_entry<C, I, R, MODE>()), ...);
-  ((t.ho[I] = ho_entry<C, I, R, MODE>()), ...);
-  ((t.to[I] = to_entry<C, I, R, MODE>()), ...);
+  ((t.th[I] = th_entry<C, I, R, MODE, VIRT>()), ...);
+  ((t.ho[I] = ho_entry<C, I, R, MODE, VIRT>()), ...);
+  ((t.to[I] = to_entry<C, I, R, MODE, VIRT>()), ...);
 }
 
 }  // namespace b200

@@ -149,6 +149,8 @@ struct PlanOptions {
   double cluster_cost = 0.05;  // the DSMEM exchange, in passes
   int mid_lrun = 5;            // shortest run of a middle pass (k >= 24 plans)
   int regbits14 = 0;           // keys per thread of the 14-bit merge passes (0 = as R)
+  int tile_c = 0;              // tile-sort size for single arrays (0 = per-size default)
+  bool virt = false;           // virtual-padding plan: 2^13-key cosets only, 32 keys/thread
 };
 
 inline int ctz64(uint64_t x) {
@@ -189,6 +191,12 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   } else {
     C = 13;
   }
+  if (opt.tile_c > 0 && opt.cmin != opt.cmax && batch == 1 && k > opt.tile_c) C = opt.tile_c;
+  if (opt.virt) {
+    // the virtual-padding kernels exist for 2^13-key tiles and cosets only
+    if (k < 14 || batch != 1 || opt.kv) throw std::invalid_argument("virtual plan needs k >= 14");
+    C = 13;
+  }
   if (C > opt.cmax) C = opt.cmax > k ? k : opt.cmax;
   if (batch > 1) {
     // Batched arrays of >= 2^8 keys: one array per CTA (the specialised
@@ -225,6 +233,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   // (measured on B200).
   int R = opt.regbits > 0 ? opt.regbits
                           : ((k <= 21 && batch == 1) || (batch > 1 && C >= 10 && C <= 14) ? 4 : 5);
+  if (opt.virt) R = 5;
   if (opt.kv) R = C < 4 ? C : 4;
   for (auto& q : plan) q.R = R;
   if (opt.tile_regbits > 0 && !opt.kv) plan.front().R = opt.tile_regbits;
@@ -241,6 +250,7 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
   const int CT = C;
   int cm = opt.cmerge;
   if (cm == 0 && opt.cmin != opt.cmax && k >= 24) cm = 14;
+  if (opt.virt) cm = 13;
   // (cm <= C + 2: the first merge state, phase C+1 from bit C, must have its
   // direction bit at or above local bit cm-1 -- see the tail-only / tail+head
   // rules in the DP below.)
@@ -297,19 +307,25 @@ inline std::vector<PlanPass> make_plan(int k, uint64_t batch,
     std::vector<int> choice((size_t)K * K, 0);  // 0 tail-only, >0 tail+head h, <0 middle -h
     std::vector<int> choice_c((size_t)K * K, C);
     std::vector<char> choice_cl((size_t)K * K, 0);
-    const bool use_cluster = opt.cluster && !opt.kv && batch == 1 && k >= opt.cluster_min_k &&
+    const bool use_cluster = opt.cluster && !opt.virt && !opt.kv && batch == 1 && k >= opt.cluster_min_k &&
                              C >= 14 && !(opt.cmin == opt.cmax);
-    const int mid_lrun = (!opt.kv && batch == 1 && k >= opt.cluster_min_k &&
+    const int mid_lrun = (!opt.kv && !opt.virt && batch == 1 && k >= opt.cluster_min_k &&
                           !(opt.cmin == opt.cmax)) ? std::min(opt.mid_lrun, lrun) : lrun;
     std::vector<int> cands = {C};
     if (opt.mixed_c && CT < C && CT >= 12)
       for (int c = C - 1; c >= CT; --c) cands.push_back(c);
+    if (opt.mixed_c && CT == C && C == 14 && opt.tile_c == 14) cands.push_back(13);
     // measured best on B200: 0.3 up to 2^26 keys, 0.2 for 2^27..2^28, 0.1 above
     const double wide_tail = opt.wide_tail_cost >= 0 ? opt.wide_tail_cost
                              : (k <= 26 ? 0.3 : (k <= 28 ? 0.2 : 0.1));
     auto cost_of = [&](int Cc, int SA, int SB) {
       double c = 1.0 + opt.trip_cost * (detail::merge_trips(Cc, R, SA, SB) - 1);
-      if (Cc > CT && SA >= 0) c += wide_tail * (Cc - CT);
+      // (wide tail passes run fewer CTAs per SM: charged against the tile's
+      // coset size; with a 14-bit tile, against the 13-bit alternative)
+      if (SA >= 0) {
+        if (Cc > CT) c += wide_tail * (Cc - CT);
+        else if (opt.tile_c == 14 && Cc == 14) c += wide_tail;
+      }
       return c;
     };
     std::function<double(int, int)> solve = [&](int p, int b) -> double {

@@ -61,7 +61,8 @@ struct GraphKey {
   uint32_t kx;
   int cmax, cmin, lrun, regbits, tile_regbits, cmerge, dp, generic, pdl;
   double trip_cost, wide_tail_cost, cluster_cost;
-  int mixed_c, cluster, mid_lrun, regbits14;
+  int mixed_c, cluster, mid_lrun, regbits14, tile_c;
+  uint64_t nreal;  // virtual padding: real keys (0 = none)
   bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 // An instantiated graph is shared between the cache and every caller that is
@@ -148,7 +149,7 @@ void release_multi_ctx();
 // words are d_keys (mode 2).
 int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
               uint32_t key_xor, cudaStream_t stream, int only = -1,
-              uint32_t* d_vals = nullptr, int mode = -1);
+              uint32_t* d_vals = nullptr, int mode = -1, uint64_t nreal = 0);
 // Output window [o_begin, o_begin + o_len) of merge(A[0..la), B[0..lb)).
 int merge_window_impl(const uint32_t* A, uint64_t la, const uint32_t* B, uint64_t lb,
                       uint64_t o_begin, uint64_t o_len, uint32_t key_xor, uint32_t* out,

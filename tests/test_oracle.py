@@ -185,3 +185,53 @@ def test_oracle_at_2_24_matches_reference_digest(orc, golden):
     x = orc.generate_input(1 << 24, 1)
     assert h(orc.fnv1a64(x)) == c["input_fnv"]
     assert h(orc.fnv1a64(orc.quicksort_u32(x))) == c["u32_asc_fnv"]
+
+
+def _network_virtual(x, k, nreal, X=None):
+    """The bitonic network on 2^k slots with slots >= nreal virtual (+inf)
+    and the virtual plans' direction rule (phase p descending iff bit p of
+    i ^ (nreal - 1) is set).  Returns the output and whether any
+    compare-exchange moved a real key into a virtual slot."""
+    n = 1 << k
+    a = np.full(n, 0xFFFFFFFF, dtype=np.uint64)
+    a[:nreal] = x
+    X = nreal - 1 if X is None else X
+    leaked = False
+    idx = np.arange(n)
+    for p in range(1, k + 1):
+        for s in range(p - 1, -1, -1):
+            lo = idx[(idx >> s) & 1 == 0]
+            hi = lo | (1 << s)
+            desc = ((lo ^ X) >> p) & 1 if p < k else np.zeros_like(lo)
+            x0, x1 = a[lo], a[hi]
+            mn, mx = np.minimum(x0, x1), np.maximum(x0, x1)
+            new_lo = np.where(desc == 1, mx, mn)
+            new_hi = np.where(desc == 1, mn, mx)
+            # a real key (index < nreal) must never land on a virtual slot
+            moved = (hi >= nreal) & (new_hi != 0xFFFFFFFF)
+            leaked |= bool(moved.any())
+            a[lo], a[hi] = new_lo, new_hi
+    return a[:nreal].astype(np.uint32), leaked
+
+
+@pytest.mark.parametrize("k", [3, 5, 8, 11])
+def test_virtual_padding_direction_rule(k):
+    """Virtual padding (no padded copy) is exact: with the direction rule of
+    the virtual plans, no compare-exchange ever moves a real key into a
+    virtual slot, for every length 2^(k-1) < n <= 2^k, and the real prefix
+    comes out sorted (bench.cpp:366-377's pad + sort + truncate)."""
+    rng = np.random.default_rng(k)
+    ns = range((1 << (k - 1)) + 1, (1 << k) + 1) if k <= 8 else \
+        sorted(set(rng.integers((1 << (k - 1)) + 1, (1 << k) + 1, 40).tolist()))
+    for n in ns:
+        x = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+        x[: n // 5] = 0xFFFFFFFF  # real keys equal to the padding value
+        got, leaked = _network_virtual(x, k, n)
+        assert not leaked, n
+        assert (got == np.sort(x)).all(), n
+    # with the standard rule (X = 0) real keys do leak into the padding:
+    # the direction rule is what makes the copy unnecessary
+    n = (1 << k) - 3
+    x = rng.integers(0, 2**31, n, dtype=np.uint64).astype(np.uint32)
+    _, leaked = _network_virtual(x, k, n, X=0)
+    assert leaked

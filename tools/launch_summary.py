@@ -24,8 +24,13 @@ def load(path):
 
 
 def family(name):
-    return "tile_sort" if "tile_sort_kernel" in name else (
-        "merge" if "merge_kernel" in name else name.split("(")[0].split()[-1])
+    if "tile_sort" in name:
+        return "tile_sort"
+    if "merge_bitonic_kernel" in name:
+        return "merge_path"  # the merge-path tiles (multi-GPU / host entry)
+    if "merge_kernel" in name or "cluster_merge" in name:
+        return "merge"
+    return name.split("(")[0].split()[-1]
 
 
 def summarise(path):

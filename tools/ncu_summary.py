@@ -27,3 +27,32 @@ for row in r[2:]:
             try: st.append((float(v), h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")))
             except: pass
     print("  stalls/issue:", ", ".join("%s=%.2f" % (n, v) for v, n in sorted(st, reverse=True)[:8]))
+
+# Source-level shared-memory check: per kernel, the L1 shared wavefronts the
+# SASS instructions executed vs the ideal (conflict-free) count.  The raw
+# l1tex__data_bank_conflicts_* counter also counts arbitration between
+# different instructions; this one is per instruction.
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+name, hdr2, tot = None, None, collections.OrderedDict()
+for row in csv.reader(io.StringIO(src)):
+    if row and row[0] == "Kernel Name":
+        name, hdr2 = row[1], None
+        continue
+    if row and row[0] == "Address":
+        hdr2 = row
+        continue
+    if hdr2 and name and len(row) == len(hdr2):
+        d = dict(zip(hdr2, row))
+        try:
+            w = float(d.get("L1 Wavefronts Shared") or 0)
+            i = float(d.get("L1 Wavefronts Shared Ideal") or 0)
+        except ValueError:
+            continue
+        t = tot.setdefault(name, [0.0, 0.0])
+        t[0] += w
+        t[1] += i
+if tot:
+    print("=== shared-memory wavefronts per SASS instruction (source page): executed / ideal")
+    for k, (w, i) in tot.items():
+        print("  %-70s %14.0f / %14.0f  (excess %.3f%%)" % (k[:70], w, i, 100.0 * (w - i) / i if i else 0.0))
