@@ -296,6 +296,7 @@ struct PlanKey {
   double trip_cost;
   bool mixed_c;
   double wide_tail_cost;
+  bool virt;
   bool cluster;
   double cluster_cost;
   int mid_lrun, regbits14, tile_c;
@@ -304,7 +305,7 @@ struct PlanKey {
            lrun == o.lrun && min_ctas == o.min_ctas && regbits == o.regbits && dp == o.dp &&
            kv == o.kv && tile_regbits == o.tile_regbits && cmerge == o.cmerge &&
            trip_cost == o.trip_cost && mixed_c == o.mixed_c &&
-           wide_tail_cost == o.wide_tail_cost && cluster == o.cluster &&
+           wide_tail_cost == o.wide_tail_cost && virt == o.virt && cluster == o.cluster &&
            cluster_cost == o.cluster_cost && mid_lrun == o.mid_lrun &&
            regbits14 == o.regbits14 && tile_c == o.tile_c;
   }
@@ -314,7 +315,7 @@ std::vector<std::pair<PlanKey, std::vector<b200::PlanPass>>> g_plans;
 std::vector<b200::PlanPass> cached_plan(int k, uint64_t batch, const b200::PlanOptions& o) {
   const PlanKey key{k, batch, o.cmax, o.cmin, o.lrun, o.min_ctas, o.regbits, o.tile_regbits,
                     o.cmerge, o.dp, o.kv, o.trip_cost, o.mixed_c, o.wide_tail_cost,
-                    o.cluster, o.cluster_cost, o.mid_lrun, o.regbits14, o.tile_c};
+                    o.virt, o.cluster, o.cluster_cost, o.mid_lrun, o.regbits14, o.tile_c};
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (auto& e : g_plans)
     if (e.first == key) return e.second;
@@ -402,7 +403,17 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
               uint32_t key_xor, cudaStream_t stream, int only, uint32_t* d_vals, int mode,
               uint64_t nreal) {
   if (mode < 0) mode = d_vals != nullptr ? 1 : 0;
-  const bool virt = nreal != 0 && nreal < n_per;
+  bool virt = nreal != 0 && nreal < n_per;
+  // testing aid: B200_BITONIC_VIRT_DEBUG=<dxor> runs a power-of-two sort
+  // through the virtual-padding kernels (nreal = n, the given direction xor)
+  uint64_t dbg_dxor = ~uint64_t{0};
+  if (const char* e = std::getenv("B200_BITONIC_VIRT_DEBUG")) {
+    if (!virt && batch == 1 && d_vals == nullptr && mode == 0) {
+      virt = true;
+      nreal = n_per;
+      dbg_dxor = std::strtoull(e, nullptr, 0);
+    }
+  }
   if (virt && (batch != 1 || d_vals != nullptr || mode != 0)) {
     return fail(B200_CONFIG, "virtual padding: single key-only arrays");
   }
@@ -464,7 +475,7 @@ int sort_impl(uint32_t* d_keys, uint64_t n_per, uint64_t batch, int descending,
       p.mone = 0xFFFFFFFFu;
       p.reverse = (reverse_enabled() && (i & 1) && !q.cluster) ? 1 : 0;
       p.nreal = virt ? nreal : ~uint64_t{0};
-      p.dxor = virt ? nreal - 1 : 0;
+      p.dxor = virt ? (dbg_dxor != ~uint64_t{0} ? dbg_dxor : nreal - 1) : 0;
       cudaError_t e = launch_pass(q, p, st, virt ? 3 : mode);
       if (e == cudaErrorNotSupported) {
         return fail(B200_CONFIG,
@@ -578,9 +589,16 @@ __global__ void pad_fill_kernel(uint32_t* dst, const uint32_t* src, uint64_t n,
   }
 }
 
-bool virtual_padding_disabled() {
+// Virtual padding from 2^26 padded keys (B200: 2^28 - 1 keys 11.98 vs
+// 11.97 ms with the copy, 0.81 x 2^28 keys 10.73 vs 11.86 ms, and no 1 GiB
+// scratch; below that the copy path's size-tuned plans win, e.g. 2^20 - 1
+// keys 0.075 vs 0.141 ms).  B200_BITONIC_VIRTUAL=1 forces it from 2^15
+// (tests), =0 disables it.
+bool use_virtual_padding(uint64_t m) {
   const char* e = std::getenv("B200_BITONIC_VIRTUAL");
-  return e && std::strcmp(e, "0") == 0;
+  if (e && std::strcmp(e, "0") == 0) return false;
+  if (e && std::strcmp(e, "1") == 0) return m >= (uint64_t{1} << 15);
+  return m >= (uint64_t{1} << 26);
 }
 
 int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
@@ -621,7 +639,7 @@ int padded_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
     cudaFreeAsync(out, s);
     return rc;
   }
-  if (aligned && m >= (uint64_t{1} << 15) && !virtual_padding_disabled()) {
+  if (aligned && use_virtual_padding(m)) {
     // Virtual padding: the 2^j-key network runs in place on the n real keys;
     // the m - n virtual keys are never loaded or stored (bitonic_static.cuh,
     // VIRT kernels) -- no scratch copy, no copy back.

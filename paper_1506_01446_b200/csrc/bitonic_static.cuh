@@ -145,13 +145,22 @@ __device__ __forceinline__ void stage_in(uint32_t* sm, const uint32_t* keys,
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const uint32_t j = j0 + (uint32_t)(it * 4 * T);
-      uint32_t m = m_uniform;
-      if constexpr (DBIT >= 0) m ^= 0u - ((j >> DBIT) & 1u);
       const uint32_t pj = TL::pad(j);
-      sm[pj + 0] = buf[it].x ^ m;
-      sm[pj + 1] = buf[it].y ^ m;
-      sm[pj + 2] = buf[it].z ^ m;
-      sm[pj + 3] = buf[it].w ^ m;
+      if constexpr (DBIT >= 0 && DBIT < 2) {
+        // the direction bit varies inside the 4-key vector (the virtual
+        // tile sort's phase-1 domain): one mask per key
+        sm[pj + 0] = buf[it].x ^ m_uniform ^ (0u - (((j + 0u) >> DBIT) & 1u));
+        sm[pj + 1] = buf[it].y ^ m_uniform ^ (0u - (((j + 1u) >> DBIT) & 1u));
+        sm[pj + 2] = buf[it].z ^ m_uniform ^ (0u - (((j + 2u) >> DBIT) & 1u));
+        sm[pj + 3] = buf[it].w ^ m_uniform ^ (0u - (((j + 3u) >> DBIT) & 1u));
+      } else {
+        uint32_t m = m_uniform;
+        if constexpr (DBIT >= 0) m ^= 0u - ((j >> DBIT) & 1u);
+        sm[pj + 0] = buf[it].x ^ m;
+        sm[pj + 1] = buf[it].y ^ m;
+        sm[pj + 2] = buf[it].z ^ m;
+        sm[pj + 3] = buf[it].w ^ m;
+      }
     }
   } else {
     for (uint32_t j = threadIdx.x; j < (uint32_t)N; j += T) {

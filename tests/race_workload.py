@@ -118,6 +118,16 @@ b.sort_padded_(t)
 torch.cuda.synchronize()
 check("padded 2^16+5", host(t), np.sort(x))
 
+# virtual padding (forced below its 2^26 default threshold): partial cosets
+os.environ["B200_BITONIC_VIRTUAL"] = "1"
+for n in [(1 << 16) - 12345, (1 << 18) - 3]:
+    x = u32(n)
+    t = dev_t(x)
+    b.sort_padded_(t)
+    torch.cuda.synchronize()
+    check(f"virtual padding {n}", host(t), np.sort(x))
+os.environ.pop("B200_BITONIC_VIRTUAL")
+
 # pipelined host entry (4 chunks, merge tree, windowed D2H), pinned twice
 os.environ["B200_BITONIC_HOST_CHUNKS"] = "4"
 x = u32(1 << 18)
