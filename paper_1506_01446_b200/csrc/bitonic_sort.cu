@@ -502,12 +502,26 @@ int merge_window_impl(const uint32_t* A, uint64_t la, const uint32_t* B, uint64_
   b200::merge_partition_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
       A, la, B, lb, o_begin, o_len, key_xor, scratch_coranks, nb);
   constexpr int C = b200::kMergeC;
-  const void* fn = reinterpret_cast<const void*>(&b200::merge_bitonic_kernel<C>);
-  cudaError_t e = ensure_attr(fn, C, 1);
-  if (e != cudaSuccess) return cuda_fail(e, "merge kernel attribute");
-  b200::merge_bitonic_kernel<C><<<(unsigned)tiles, b200::threads_for<C, 5>(),
-                                  b200::tile_smem_words(C) * 4, s>>>(
-      A, B, o_begin, o_len, key_xor, scratch_coranks, out, 1u, 0xFFFFFFFFu);
+  static const int mr = [] {  // keys per thread of the merge tiles (experiment knob)
+    const char* e = std::getenv("B200_BITONIC_MERGE_R");
+    return e ? std::atoi(e) : 5;
+  }();
+  cudaError_t e;
+  if (mr == 4) {
+    const void* fn = reinterpret_cast<const void*>(&b200::merge_bitonic_kernel<C, 4>);
+    e = ensure_attr(fn, C, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "merge kernel attribute");
+    b200::merge_bitonic_kernel<C, 4><<<(unsigned)tiles, b200::threads_for<C, 4>(),
+                                       b200::tile_smem_words(C) * 4, s>>>(
+        A, B, o_begin, o_len, key_xor, scratch_coranks, out, 1u, 0xFFFFFFFFu);
+  } else {
+    const void* fn = reinterpret_cast<const void*>(&b200::merge_bitonic_kernel<C>);
+    e = ensure_attr(fn, C, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "merge kernel attribute");
+    b200::merge_bitonic_kernel<C><<<(unsigned)tiles, b200::threads_for<C, 5>(),
+                                    b200::tile_smem_words(C) * 4, s>>>(
+        A, B, o_begin, o_len, key_xor, scratch_coranks, out, 1u, 0xFFFFFFFFu);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "merge launch");
   return B200_OK;

@@ -68,7 +68,7 @@ __global__ void merge_partition_kernel(const uint32_t* __restrict__ A, uint64_t 
 // maximum between the two runs (keeping it bitonic); the padding sorts to
 // the end and is not stored.
 template <int C = kMergeC, int R = 5>
-__global__ void __launch_bounds__(threads_for<C, R>(), 3)  // 85 registers: 32 loads in flight
+__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
 merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
                      uint64_t o_begin, uint64_t o_len, uint32_t kx,
                      const uint64_t* __restrict__ coranks, uint32_t* __restrict__ out,
@@ -84,62 +84,9 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
   const uint64_t j1 = o_begin + o1 - i1;
   const int na = (int)(i1 - i0);
   const int L = (int)(o1 - o0);
-  // stage: local j -> A[i0 + j] (j < na, ascending), padding (the maximum),
-  // B backwards in the last nb slots (descending): ascending, flat,
-  // descending is bitonic.  All of a thread's loads are issued before the
-  // first store (memory-level parallelism).
-  {
-    // 16-byte loads on the aligned interior of both windows (the edges, at
-    // most 3 + 3 keys per window, and the padding are stored separately).
-    // Chunk u of the concatenated chunk list is A chunk u or B chunk u-nA4;
-    // each thread issues all its chunk loads before any store.
-    const int nbk = L - na;
-    const uint64_t j0 = j1 - (uint64_t)nbk;
-    const uint64_t a0 = (i0 + 3) & ~uint64_t{3}, a1e = i1 & ~uint64_t{3};
-    const uint64_t b0 = (j0 + 3) & ~uint64_t{3}, b1e = j1 & ~uint64_t{3};
-    const bool va = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && a1e > a0 && a0 <= i1;
-    const bool vb = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && b1e > b0 && b0 <= j1;
-    const int nA4 = va ? (int)((a1e - a0) >> 2) : 0;
-    const int nB4 = vb ? (int)((b1e - b0) >> 2) : 0;
-    constexpr int Q = N / 4 / T;  // chunk slots per thread
-    uint4 x[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int u = threadIdx.x + q * T;
-      const uint4* src = u < nA4 ? reinterpret_cast<const uint4*>(A + a0) + u
-                                 : reinterpret_cast<const uint4*>(B + b0) + (u - nA4);
-      if (u < nA4 + nB4) x[q] = __ldg(src);
-    }
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int u = threadIdx.x + q * T;
-      if (u < nA4) {
-        const uint32_t j = (uint32_t)(a0 - i0) + 4u * (uint32_t)u;  // A slot
-        smem[smem_pad(j)] = x[q].x ^ kx;
-        smem[smem_pad(j + 1)] = x[q].y ^ kx;
-        smem[smem_pad(j + 2)] = x[q].z ^ kx;
-        smem[smem_pad(j + 3)] = x[q].w ^ kx;
-      } else if (u < nA4 + nB4) {
-        // B[g] -> slot N - 1 - (g - j0)
-        const uint32_t j = (uint32_t)(N - 1) - (uint32_t)(b0 - j0) - 4u * (uint32_t)(u - nA4);
-        smem[smem_pad(j)] = x[q].x ^ kx;
-        smem[smem_pad(j - 1)] = x[q].y ^ kx;
-        smem[smem_pad(j - 2)] = x[q].z ^ kx;
-        smem[smem_pad(j - 3)] = x[q].w ^ kx;
-      }
-    }
-    // edges (keys outside the 16-byte interiors) and padding
-    const uint64_t ea0 = va ? a0 : i1, ea1 = va ? a1e : i1;  // A interior [ea0, ea1)
-    const uint64_t eb0 = vb ? b0 : j1, eb1 = vb ? b1e : j1;
-    for (uint64_t g = i0 + threadIdx.x; g < ea0; g += T) smem[smem_pad((uint32_t)(g - i0))] = A[g] ^ kx;
-    for (uint64_t g = ea1 + threadIdx.x; g < i1; g += T) smem[smem_pad((uint32_t)(g - i0))] = A[g] ^ kx;
-    for (uint64_t g = j0 + threadIdx.x; g < eb0; g += T)
-      smem[smem_pad((uint32_t)(N - 1) - (uint32_t)(g - j0))] = B[g] ^ kx;
-    for (uint64_t g = eb1 + threadIdx.x; g < j1; g += T)
-      smem[smem_pad((uint32_t)(N - 1) - (uint32_t)(g - j0))] = B[g] ^ kx;
-    for (int j = na + threadIdx.x; j < N - nbk; j += T) smem[smem_pad((uint32_t)j)] = 0xFFFFFFFFu;
-  }
-  __syncthreads();
+  // Slot j of the tile: A[i0 + j] for j < na (ascending), the maximum for
+  // the padding, B backwards in the last nb slots (descending): ascending,
+  // flat, descending is bitonic.
   typename Body::Ctx cx;
   cx.keys = out;
   cx.vals = nullptr;
@@ -148,9 +95,92 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
   cx.uA = cx.uB = cx.uC = 0u;  // one ascending phase, no direction bit
   cx.gin = cx.gout = cx.gin_lo = cx.gout_lo = 0u;
   cx.fs = FmaSplit{one, mone};
+  using L0 = typename Body::template L<0>;
   uint32_t v[1 << R];
   uint32_t w[1 << R];
-  Body::template L<0>::lds(smem, v);
+  if constexpr (Body::template direct_ok<L0>()) {
+    // Round 0's lanes own 32 consecutive slots: each register is one
+    // coalesced (possibly misaligned) warp load straight from A or B into
+    // the first round's layout -- no staging copy, no barrier.
+    const int nbk = L - na;
+    const uint32_t* pa = A + i0;                    // slot j < na        -> pa[j]
+    const uint32_t* pb = B + (j1 - 1) + (N - nbk);  // slot j >= N - nbk -> pb[-j]
+    const uint32_t tj = L0::thread_j();
+    static_assert(L0::tpos(0) == 0 && L0::tpos(4) == 4, "round 0: lanes on local bits 0..4");
+    const int lane = (int)(tj & 31u);
+    const uint32_t wbase = tj & ~31u;  // the warp's part of the slot index
+#pragma unroll
+    for (int e = 0; e < (1 << R); ++e) {
+      // a register's 32 slots are consecutive: classify the chunk once per
+      // warp (uniform branches); only the <= 2 chunks that straddle a window
+      // edge select per lane
+      const int J = (int)(wbase | L0::dep_reg(e));
+      const int j = J + lane;
+      uint32_t x;
+      if (J + 32 <= na) {
+        x = __ldg(pa + j);
+      } else if (J >= N - nbk) {
+        x = __ldg(pb - j);
+      } else {
+        x = j < na ? __ldg(pa + j) : (j >= N - nbk ? __ldg(pb - j) : ~kx);
+      }
+      v[e] = x ^ kx;
+    }
+  } else {
+  {
+      // 16-byte loads on the aligned interior of both windows (the edges, at
+      // most 3 + 3 keys per window, and the padding are stored separately).
+      // Chunk u of the concatenated chunk list is A chunk u or B chunk u-nA4;
+      // each thread issues all its chunk loads before any store.
+      const int nbk = L - na;
+      const uint64_t j0 = j1 - (uint64_t)nbk;
+      const uint64_t a0 = (i0 + 3) & ~uint64_t{3}, a1e = i1 & ~uint64_t{3};
+      const uint64_t b0 = (j0 + 3) & ~uint64_t{3}, b1e = j1 & ~uint64_t{3};
+      const bool va = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && a1e > a0 && a0 <= i1;
+      const bool vb = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && b1e > b0 && b0 <= j1;
+      const int nA4 = va ? (int)((a1e - a0) >> 2) : 0;
+      const int nB4 = vb ? (int)((b1e - b0) >> 2) : 0;
+      constexpr int Q = N / 4 / T;  // chunk slots per thread
+      uint4 x[Q];
+  #pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int u = threadIdx.x + q * T;
+        const uint4* src = u < nA4 ? reinterpret_cast<const uint4*>(A + a0) + u
+                                   : reinterpret_cast<const uint4*>(B + b0) + (u - nA4);
+        if (u < nA4 + nB4) x[q] = __ldg(src);
+      }
+  #pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int u = threadIdx.x + q * T;
+        if (u < nA4) {
+          const uint32_t j = (uint32_t)(a0 - i0) + 4u * (uint32_t)u;  // A slot
+          smem[smem_pad(j)] = x[q].x ^ kx;
+          smem[smem_pad(j + 1)] = x[q].y ^ kx;
+          smem[smem_pad(j + 2)] = x[q].z ^ kx;
+          smem[smem_pad(j + 3)] = x[q].w ^ kx;
+        } else if (u < nA4 + nB4) {
+          // B[g] -> slot N - 1 - (g - j0)
+          const uint32_t j = (uint32_t)(N - 1) - (uint32_t)(b0 - j0) - 4u * (uint32_t)(u - nA4);
+          smem[smem_pad(j)] = x[q].x ^ kx;
+          smem[smem_pad(j - 1)] = x[q].y ^ kx;
+          smem[smem_pad(j - 2)] = x[q].z ^ kx;
+          smem[smem_pad(j - 3)] = x[q].w ^ kx;
+        }
+      }
+      // edges (keys outside the 16-byte interiors) and padding
+      const uint64_t ea0 = va ? a0 : i1, ea1 = va ? a1e : i1;  // A interior [ea0, ea1)
+      const uint64_t eb0 = vb ? b0 : j1, eb1 = vb ? b1e : j1;
+      for (uint64_t g = i0 + threadIdx.x; g < ea0; g += T) smem[smem_pad((uint32_t)(g - i0))] = A[g] ^ kx;
+      for (uint64_t g = ea1 + threadIdx.x; g < i1; g += T) smem[smem_pad((uint32_t)(g - i0))] = A[g] ^ kx;
+      for (uint64_t g = j0 + threadIdx.x; g < eb0; g += T)
+        smem[smem_pad((uint32_t)(N - 1) - (uint32_t)(g - j0))] = B[g] ^ kx;
+      for (uint64_t g = eb1 + threadIdx.x; g < j1; g += T)
+        smem[smem_pad((uint32_t)(N - 1) - (uint32_t)(g - j0))] = B[g] ^ kx;
+      for (int j = na + threadIdx.x; j < N - nbk; j += T) smem[smem_pad((uint32_t)j)] = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    L0::lds(smem, v);
+  }
   Body::template rounds<0>(cx, smem, v, w);
   Body::tail(cx, v, w);
   using LL = typename Body::template L<Body::NRE - 1>;
