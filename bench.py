@@ -51,6 +51,10 @@ MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 METRIC = "Gkeys/s sorting uint32 (device-timed) vs HBM roofline; speedup vs CPU quicksort"
 SEED = 1  # generate_input's default seed (bench.cpp:354, BenchConfig)
+# The paper's published numbers for this path (Table 1
+# "GPU Optimized", Kepler K10), as Gkeys/s per log2 size.
+PAPER_GKEYS = {17: 0.364, 18: 0.397, 19: 0.400, 20: 0.375, 21: 0.357, 22: 0.341,
+               23: 0.318, 24: 0.298, 25: 0.278, 26: 0.259, 27: 0.243, 28: 0.227}
 # P_min(k, c=15): minimum HBM round trips of the network.
 PMIN = {16: 3, 20: 7, 24: 13, 28: 21, 29: 22, 30: 24, 31: 27, 32: 29}
 
@@ -833,11 +837,18 @@ def main():
                 multi["one_gpu_error"] = repr(ex)[:200]
         barrier()
 
+    # vs_baseline: the paper's own Table-1 GPU number for this exact size (K10)
+    vs_base = None
+    if world == 1 and not batched and args.log2n in PAPER_GKEYS:
+        vs_base = value / PAPER_GKEYS[args.log2n]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": vs_base,
+            "vs_baseline_source": ("paper Table 1, GPU Optimized on a Kepler K10 at this size "
+                                   "(BASELINE.md section 1, PAPER.md:96-107)"
+                                   if vs_base is not None else None),
             "dtype": "u32", "data": "synthetic", "config": cfg,
             "timing": {"l2_flush": "256 MiB write before every step (outside timing)",
                        "input_restore": "D2D copy before every step (outside timing)",
