@@ -138,8 +138,10 @@ int b200_bitonic_sort_padded_i32(int32_t* d_keys, uint64_t n, int descending,
 /* Host-memory convenience entries: H2D copy, sort, D2H copy, synchronous.
  * Mirror sequential_bitonic_sort(std::span<int32_t>) exactly (in place on
  * caller-owned host memory).  Device buffers: one block of 8 bytes per key
- * per device, grown on demand and kept for later calls (after a 2^30-key
- * sort that is 8 GiB); b200_bitonic_release_scratch frees it. */
+ * per pipeline context, grown on demand and kept for later calls (after a
+ * 2^30-key sort that is 8 GiB); concurrent callers on one device get their
+ * own context (up to 4, then they queue); b200_bitonic_release_scratch
+ * frees the blocks. */
 int b200_bitonic_sort_host_i32(int32_t* h_keys, uint64_t n, int descending);
 int b200_bitonic_sort_host_u32(uint32_t* h_keys, uint64_t n, int descending);
 

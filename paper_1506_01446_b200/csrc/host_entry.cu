@@ -29,13 +29,34 @@ struct HostPipe {
   size_t cap = 0;
 };
 std::mutex g_pipe_mu;
-std::vector<HostPipe*> g_pipes;
+std::vector<std::vector<HostPipe*>> g_pipes;  // per device; live for the process
+constexpr int kMaxPipesPerDevice = 4;
 
-HostPipe* host_pipe(int dev) {
-  std::lock_guard<std::mutex> lk(g_pipe_mu);
-  if ((int)g_pipes.size() <= dev) g_pipes.resize(dev + 1, nullptr);
-  if (g_pipes[dev] == nullptr) g_pipes[dev] = new HostPipe();  // lives for the process
-  return g_pipes[dev];
+// A free pipeline context of device `dev`, returned locked: concurrent host
+// sorts on one device each get their own buffers and streams (up to
+// kMaxPipesPerDevice, then they queue on the first).
+HostPipe* host_pipe(int dev, std::unique_lock<std::mutex>& held) {
+  HostPipe* wait_on = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    if ((int)g_pipes.size() <= dev) g_pipes.resize(dev + 1);
+    auto& v = g_pipes[dev];
+    for (HostPipe* hp : v) {
+      std::unique_lock<std::mutex> t(hp->mu, std::try_to_lock);
+      if (t.owns_lock()) {
+        held = std::move(t);
+        return hp;
+      }
+    }
+    if ((int)v.size() < kMaxPipesPerDevice) {
+      v.push_back(new HostPipe());
+      held = std::unique_lock<std::mutex>(v.back()->mu);
+      return v.back();
+    }
+    wait_on = v.front();
+  }
+  held = std::unique_lock<std::mutex>(wait_on->mu);
+  return wait_on;
 }
 
 cudaError_t pipe_init(HostPipe& P) {
@@ -96,8 +117,8 @@ int host_sort(uint32_t* h, uint64_t n, int descending, uint32_t key_xor) {
   }
   int dev = 0;
   B200_CUDA_TRY(cudaGetDevice(&dev));
-  HostPipe& P = *host_pipe(dev);
-  std::lock_guard<std::mutex> lk(P.mu);
+  std::unique_lock<std::mutex> lk;
+  HostPipe& P = *host_pipe(dev, lk);
   B200_CUDA_TRY(pipe_init(P));
   const int G = pipe_chunks(n);
   const uint64_t c = n / G;
@@ -216,13 +237,15 @@ int b200_bitonic_release_scratch(void) {
   release_multi_ctx();
   {
     std::lock_guard<std::mutex> lk(g_pipe_mu);
-    for (HostPipe* hp : g_pipes) {
-      if (hp == nullptr || hp->block == nullptr) continue;
-      std::lock_guard<std::mutex> lk2(hp->mu);
-      if (hp->init) cudaStreamSynchronize(hp->comp[0]);
-      cudaFree(hp->block);
-      hp->block = nullptr;
-      hp->cap = 0;
+    for (auto& dv : g_pipes) {
+      for (HostPipe* hp : dv) {
+        if (hp == nullptr || hp->block == nullptr) continue;
+        std::lock_guard<std::mutex> lk2(hp->mu);
+        if (hp->init) cudaStreamSynchronize(hp->comp[0]);
+        cudaFree(hp->block);
+        hp->block = nullptr;
+        hp->cap = 0;
+      }
     }
   }
   const cudaError_t e = trim_scratch_pools();
