@@ -471,6 +471,8 @@ def main():
     ap.add_argument("--batched", type=int, default=0,
                     help="n_per_array for the batched config (e.g. 4096)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the merge-path variant measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     resolve_args(args)
@@ -661,6 +663,50 @@ def main():
         sort_roof = {"p_min": pm, "p_design": len(plan), "t_roof_us": t_roof * 1e6,
                      "frac": t_roof / (ms * 1e-3),
                      "definition": "P_min(k,15) x 8 B x n / measured HBM BW (SURVEY 8d)"}
+
+    # ---- the merge-path variant on the same keys (single array, k > 13) -------
+    # b200_bitonic_sort_mergepath_u32: same output bytes, one HBM pass per
+    # global phase (co-rank partitioned bitonic tile merges) instead of the
+    # network's fused half-cleaner passes.  Reported beside the headline (which
+    # stays the network, the reference's algorithm), same timing discipline.
+    variant = None
+    if world == 1 and not batched and args.log2n > 13 and not args.no_variants:
+        try:
+            vt = []
+            for i in range(args.warmup + args.steps):
+                work.copy_(src)
+                flush.zero_()
+                torch.cuda._sleep(100_000)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                b200.sort_mergepath_(work)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if i >= args.warmup:
+                    vt.append(e0.elapsed_time(e1))
+            same = bool(np.array_equal(work.view(torch.int32).cpu().numpy().view(np.uint32),
+                                       gpu_sorted))
+            vms = sum(vt) / len(vt)
+            phases = args.log2n - 13
+            tile_ms = ms * share.get("tile_sort", 0.0) if roofline else 0.0
+            phase_ms = (vms - tile_ms) / phases
+            t_roof = pmin(args.log2n) * 8 * n / (hbm * 1e9)
+            variant = {
+                "mergepath": {
+                    "value": n / (vms * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": vms,
+                    "steps": len(vt), "output_equals_network_output": same,
+                    "passes": 1 + phases,
+                    "phase": {"kernels": "mergepath_partition_kernel + mergepath_merge_kernel<13,5>",
+                              "avg_ms": phase_ms, "algorithmic_bytes": 8 * n,
+                              "achieved_gbs": 8 * n / (phase_ms * 1e-3) / 1e9,
+                              "frac": 8 * n / (phase_ms * 1e-3) / 1e9 / hbm,
+                              "method": "(step time - the network's tile-sort time) / phases"},
+                    "sort_roofline_frac": t_roof / (vms * 1e-3),
+                    "api": "b200_bitonic_sort_mergepath_u32 (device pointer, in place, "
+                           "n-key scratch from the pool)",
+                }}
+        except Exception as ex:  # pragma: no cover - report, do not fail the bench
+            variant = {"mergepath": {"error": repr(ex)[:200]}}
 
     # ---- end to end through the public API with host buffers ---------------
     # Single array: the reference-facing host entry (sort_host ->
@@ -860,6 +906,7 @@ def main():
                            **{k: v for k, v in dist_stats.items() if k != "peer_fallback"}}
                           if world > 1 else {})},
             "e2e": e2e, "roofline": roofline, "sort_roofline": sort_roof,
+            **({"variants": variant} if variant is not None else {}),
             "cpu_baseline": cpu, "clocks": sampler.summary(),
             **({"multi_gpu": multi} if multi is not None else {}),
             "gpu_launches": launches_per_step * args.steps,

@@ -65,6 +65,21 @@ int b200_bitonic_sort_u32(uint32_t* d_keys, uint64_t n, int descending,
 int b200_bitonic_sort_i32(int32_t* d_keys, uint64_t n, int descending,
                           b200_stream_t stream);
 
+/* Merge-path variant of the same sort (keys only; identical output bytes):
+ * the tile sort leaves every 2^13-key tile ascending, then each global phase
+ * p = 14..log2(n) is ONE pass -- a co-rank partition of every run pair's
+ * merge into 2^13-key output tiles (the keys the phase's large-stride
+ * half-cleaner steps would route to each tile) and the bitonic merger's last
+ * 13 steps on each tile -- ping-ponging through an n-key scratch buffer from
+ * the retained pool (log2(n) - 12 passes; 2^28: 16 against the network's
+ * 29).  n a power of two >= 2; n <= 2^13 runs the network sort.  Not part of
+ * the reference's interface: an option for callers that only need the
+ * sorted keys. */
+int b200_bitonic_sort_mergepath_u32(uint32_t* d_keys, uint64_t n, int descending,
+                                    b200_stream_t stream);
+int b200_bitonic_sort_mergepath_i32(int32_t* d_keys, uint64_t n, int descending,
+                                    b200_stream_t stream);
+
 /* `batch` independent contiguous arrays of n_per_array keys each, every one
  * sorted on its own (BASELINE config "4096 arrays of 2^12").  n_per_array
  * must be a power of two >= 2; batch >= 1. */

@@ -34,7 +34,7 @@ from . import _native
 
 __all__ = [
     "InvalidSizeError", "ConfigError", "CudaError",
-    "sort_", "sort_pairs_", "sort_planes_", "argsort", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
+    "sort_", "sort_mergepath_", "sort_pairs_", "sort_planes_", "argsort", "sort_padded_", "sort_batched_", "run_pass_", "sequential_bitonic_sort", "sort_host",
     "merge_split_", "merge_", "sort_multi", "plan", "counters", "set_tuning",
     "PassPlan", "version", "library_path", "release_scratch", "generate_input",
 ]
@@ -202,6 +202,20 @@ def sort_padded_(t, descending: bool = False, stream=None):
     kind = _key_dtype32(t)
     fn = (_native.lib().b200_bitonic_sort_padded_i32 if kind == "i32"
           else _native.lib().b200_bitonic_sort_padded_u32)
+    with _on_device(t):
+        _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
+                  ctypes.c_void_p(_stream_ptr(stream))))
+    return t
+
+
+def sort_mergepath_(t, descending: bool = False, stream=None):
+    """The merge-path variant of ``sort_`` (uint32 / int32, power-of-two
+    length): identical output, one pass per global phase (tile sort + co-rank
+    partitioned bitonic tile merges through an n-key scratch buffer)."""
+    _check_tensor(t)
+    kind = _key_dtype32(t)
+    fn = (_native.lib().b200_bitonic_sort_mergepath_i32 if kind == "i32"
+          else _native.lib().b200_bitonic_sort_mergepath_u32)
     with _on_device(t):
         _check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(bool(descending)),
                   ctypes.c_void_p(_stream_ptr(stream))))

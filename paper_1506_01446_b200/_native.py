@@ -41,6 +41,8 @@ EXPORTED = (
     "b200_bitonic_stream_wait_event",
     "b200_bitonic_sort_padded_u32",
     "b200_bitonic_sort_padded_i32",
+    "b200_bitonic_sort_mergepath_u32",
+    "b200_bitonic_sort_mergepath_i32",
     "b200_bitonic_sort_host_i32",
     "b200_bitonic_sort_host_u32",
     "b200_bitonic_generate_input",
@@ -116,6 +118,8 @@ def lib() -> ctypes.CDLL:
     L.b200_bitonic_sort_pairs_u32_batched.argtypes = [vp, vp, u64, u64, i, vp]
     L.b200_bitonic_sort_padded_u32.argtypes = [vp, u64, i, vp]
     L.b200_bitonic_sort_padded_i32.argtypes = [vp, u64, i, vp]
+    L.b200_bitonic_sort_mergepath_u32.argtypes = [vp, u64, i, vp]
+    L.b200_bitonic_sort_mergepath_i32.argtypes = [vp, u64, i, vp]
     L.b200_bitonic_sort_host_i32.argtypes = [vp, u64, i]
     L.b200_bitonic_sort_host_u32.argtypes = [vp, u64, i]
     L.b200_bitonic_generate_input.argtypes = [vp, u64, u64]

@@ -94,6 +94,9 @@ struct PassParams {
   // opposite directions, so a pass starts on the cosets the previous pass
   // wrote last -- still in L2 when the array is larger than L2.
   int reverse;
+  // Tile-sort passes only: store the sorted tiles here instead of in place
+  // (nullptr: in place).  The merge-path variant's first pass.
+  uint32_t* keys_out;
 };
 
 // Coset index of this CTA (see PassParams::reverse).

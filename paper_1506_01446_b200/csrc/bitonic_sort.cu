@@ -257,7 +257,7 @@ cudaError_t launch_tile_tma(const b200::PlanPass& q, b200::PassParams p, uint64_
 cudaError_t launch_pass(const b200::PlanPass& q, b200::PassParams p, cudaStream_t s,
                         int mode) {
   if (q.tile_sort && mode == 0 && q.R == 5 && q.p_end == q.C && tma_enabled() &&
-      !g_force_generic.load()) {
+      !g_force_generic.load() && p.keys_out == nullptr) {
     bool done = false;
     cudaError_t e = launch_tile_tma(q, p, q.ctas << q.C, s, &done);
     if (done || e != cudaSuccess) return e;
@@ -527,6 +527,99 @@ int merge_window_impl(const uint32_t* A, uint64_t la, const uint32_t* B, uint64_
   return B200_OK;
 }
 
+// ---- merge-path variant ---------------------------------------------------------
+// The same result as the network sort (keys only), with each global phase in
+// ONE HBM round trip: the tile sort leaves every 2^13-key tile ascending,
+// then phase p (p = 14..k) merges run pairs by co-rank partition + bitonic
+// tile merge (merge_split.cuh), ping-ponging between the array and one
+// n-key scratch buffer so the last phase lands in the array.  k - 12 passes
+// instead of the network's P(k) (2^28: 16 vs 29), at the price of an n-key
+// scratch buffer and of the network's intermediate states (payload order of
+// ties would differ, so key-value sorts stay on the network).
+int mergepath_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xor,
+                   cudaStream_t s) {
+  if (n < 2 || !is_pow2(n)) {
+    return fail(B200_INVALID_SIZE,
+                "length must be a power of two >= 2, got " + std::to_string(n));
+  }
+  if (descending != 0 && descending != 1) return fail(B200_CONFIG, "descending must be 0 or 1");
+  if (d_keys == nullptr) return fail(B200_CONFIG, "null key pointer");
+  constexpr int C = b200::kMergeC;
+  const int k = log2_exact(n);
+  if (k <= C || k > 34) return sort_impl(d_keys, n, 1, descending, key_xor, s);
+  if ((reinterpret_cast<uintptr_t>(d_keys) & 15u) != 0) {
+    return fail(B200_CONFIG, "device pointers must be 16-byte aligned");
+  }
+  const uint32_t kx = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+  const int phases = k - C;
+  const uint64_t tiles = n >> C;
+  uint32_t* tmp = nullptr;
+  uint64_t* cor = nullptr;
+  B200_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&tmp), n * 4, s));
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cor), (tiles + 1) * sizeof(uint64_t), s);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(tmp, s);
+    return cuda_fail(e, "scratch");
+  }
+  int rc = B200_OK;
+  // phase i (1-based) writes buf[i & 1]; the tile sort writes buf[0]
+  uint32_t* buf[2] = {(phases & 1) ? tmp : d_keys, (phases & 1) ? d_keys : tmp};
+  {
+    b200::PlanPass q;
+    q.C = C;
+    q.R = 5;
+    q.a = q.y = C;
+    q.tile_sort = 1;
+    q.p_end = C;
+    q.ctas = tiles;
+    b200::PassParams p{};
+    p.keys = d_keys;
+    p.keys_out = buf[0] == d_keys ? nullptr : buf[0];
+    p.gmask_in = p.gmask_out = kx;  // every tile ascending in the order kx selects
+    p.a = p.y = C;
+    p.kd = C;
+    p.tile_sort = 1;
+    p.p_end = C;
+    p.segA_hi = p.segB_lo = -1;
+    p.one = 1u;
+    p.mone = 0xFFFFFFFFu;
+    p.nreal = ~uint64_t{0};
+    e = launch_pass(q, p, s, 0);
+    if (e != cudaSuccess) rc = cuda_fail(e, "merge-path tile sort");
+  }
+  static const int mr = [] {  // keys per thread of the merge tiles (experiment knob)
+    const char* x = std::getenv("B200_BITONIC_MERGEPATH_R");
+    return x ? std::atoi(x) : 5;
+  }();
+  if (rc == B200_OK) {
+    const void* fn = mr == 4 ? reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C, 4>)
+                             : reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C>);
+    e = ensure_attr(fn, C, 1);
+    if (e != cudaSuccess) rc = cuda_fail(e, "merge kernel attribute");
+  }
+  for (int i = 1; i <= phases && rc == B200_OK; ++i) {
+    const uint32_t* src = buf[(i - 1) & 1];
+    uint32_t* dst = buf[i & 1];
+    const int p = C + i;
+    b200::mergepath_partition_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(
+        src, p, kx, cor, tiles);
+    if (mr == 4) {
+      b200::mergepath_merge_kernel<C, 4><<<(unsigned)tiles, b200::threads_for<C, 4>(),
+                                           b200::tile_smem_words(C) * 4, s>>>(
+          src, dst, p, kx, cor, 1u, 0xFFFFFFFFu);
+    } else {
+      b200::mergepath_merge_kernel<C><<<(unsigned)tiles, b200::threads_for<C, 5>(),
+                                        b200::tile_smem_words(C) * 4, s>>>(
+          src, dst, p, kx, cor, 1u, 0xFFFFFFFFu);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_fail(e, "merge-path phase");
+  }
+  cudaFreeAsync(cor, s);
+  cudaFreeAsync(tmp, s);
+  return rc;
+}
+
 int merge_split_impl(const uint32_t* local, const uint32_t* partner, uint64_t m,
                      int keep_high, uint32_t key_xor, uint32_t* out,
                      uint64_t* scratch_coranks, cudaStream_t s) {
@@ -750,6 +843,17 @@ int b200_bitonic_sort_u64_planes(uint32_t* d_hi, uint32_t* d_lo, uint64_t n,
   if (d_lo == nullptr) return fail(B200_CONFIG, "null low-word pointer");
   return sort_impl(d_hi, n, 1, descending, 0u, reinterpret_cast<cudaStream_t>(stream), -1,
                    d_lo, 2);
+}
+
+int b200_bitonic_sort_mergepath_u32(uint32_t* d_keys, uint64_t n, int descending,
+                                    b200_stream_t stream) {
+  return mergepath_impl(d_keys, n, descending, 0u, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200_bitonic_sort_mergepath_i32(int32_t* d_keys, uint64_t n, int descending,
+                                    b200_stream_t stream) {
+  return mergepath_impl(reinterpret_cast<uint32_t*>(d_keys), n, descending, 0x80000000u,
+                        reinterpret_cast<cudaStream_t>(stream));
 }
 
 int b200_bitonic_sort_padded_u32(uint32_t* d_keys, uint64_t n, int descending,

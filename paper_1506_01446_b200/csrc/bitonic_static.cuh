@@ -734,7 +734,15 @@ tile_sort_kernel(PassParams P) {
   } else {
     c.uC = 0u - dir_bit_global(c.gbase, C, P.kd);
   }
-  B::run(c, smem);
+  uint32_t v[B::NR];
+  uint32_t w[B::NR];
+  pdl_wait();
+  B::load(c, smem, v, w);
+  B::template rounds<0>(c, smem, v, w);
+  B::tail(c, v, w);
+  if (P.keys_out != nullptr) c.keys = P.keys_out;  // out of place (merge-path variant)
+  B::store(c, smem, v, w);
+  pdl_trigger();
 }
 
 template <int C, int SA, int SB, int R = reg_bits(C), int MODE = 0, bool VIRT = false>

@@ -67,23 +67,50 @@ __global__ void merge_partition_kernel(const uint32_t* __restrict__ A, uint64_t 
 // 2^29-key merge-split).  A partial last tile is padded with the order's
 // maximum between the two runs (keeping it bitonic); the padding sorts to
 // the end and is not stored.
-template <int C = kMergeC, int R = 5>
-__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
-merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
-                     uint64_t o_begin, uint64_t o_len, uint32_t kx,
-                     const uint64_t* __restrict__ coranks, uint32_t* __restrict__ out,
-                     uint32_t one, uint32_t mone) {
+//
+// (.nc measured faster than .lu here: 2^28 merge-path sort 7.8 vs 8.5 ms)
+#ifndef B200_MP_LD
+#define B200_MP_LD ".nc"
+#endif
+// Register e of round 0 (slot offset D = dep_reg(e) from the thread's slot):
+// A[tj + D] when D < room, else B[-(tj + D)] -- D is a compile-time immediate.
+template <int D>
+__device__ __forceinline__ uint32_t ld_split(const uint32_t* ta, const uint32_t* tb, int room) {
+  uint32_t x;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.gt.s32 p, %1, %4;\n\t"
+      "@p ld.global" B200_MP_LD ".u32 %0, [%2+%5];\n\t"
+      "@!p ld.global" B200_MP_LD ".u32 %0, [%3+%6];\n\t}"
+      : "=r"(x)
+      : "r"(room), "l"(ta), "l"(tb), "n"(D), "n"(4 * D), "n"(-4 * D));
+  return x;
+}
+
+//
+// merge_tile: the body, for one output tile o[0..L) = keys i0..i1 of A and
+// keys j1-(L-(i1-i0)) .. j1 of B (both in the order kx selects).
+template <class L0, int NR, int E = 0>
+__device__ __forceinline__ void load_full_regs(const uint32_t* ta, const uint32_t* tb, int room,
+                                               uint32_t kx, uint32_t (&v)[NR]) {
+  if constexpr (E < NR) {
+    v[E] = ld_split<(int)L0::dep_reg(E)>(ta, tb, room) ^ kx;
+    load_full_regs<L0, NR, E + 1>(ta, tb, room, kx, v);
+  }
+}
+
+template <int C, int R>
+__device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
+                                           const uint32_t* __restrict__ B, uint64_t i0,
+                                           uint64_t i1, uint64_t j1, int L, uint32_t kx,
+                                           uint32_t* __restrict__ o, uint32_t one,
+                                           uint32_t mone, uint32_t* smem) {
   using Body = PassBody<C, 1, C - 1, -1, R, 0>;
   constexpr int T = threads_for<C, R>();
   constexpr int N = 1 << C;
-  extern __shared__ uint32_t smem[];
-  const uint64_t c = blockIdx.x;
-  const uint64_t o0 = c * (uint64_t)N;
-  const uint64_t o1 = (o0 + N < o_len) ? o0 + N : o_len;
-  const uint64_t i0 = coranks[c], i1 = coranks[c + 1];
-  const uint64_t j1 = o_begin + o1 - i1;
+  const uint64_t o0 = 0;
+  uint32_t* const out = o;
   const int na = (int)(i1 - i0);
-  const int L = (int)(o1 - o0);
   // Slot j of the tile: A[i0 + j] for j < na (ascending), the maximum for
   // the padding, B backwards in the last nb slots (descending): ascending,
   // flat, descending is bitonic.
@@ -107,6 +134,16 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
     const uint32_t* pb = B + (j1 - 1) + (N - nbk);  // slot j >= N - nbk -> pb[-j]
     const uint32_t tj = L0::thread_j();
     static_assert(L0::tpos(0) == 0 && L0::tpos(4) == 4, "round 0: lanes on local bits 0..4");
+    if (L == N) {
+      // Full tile (every merge-path phase tile): no padding, slot j is A[i0+j]
+      // below na, else B backwards.  Per register one compare against an
+      // immediate and two predicated loads with immediate offsets from two
+      // per-thread bases (3 instructions; no per-register address math).
+      const uint32_t* ta = pa + tj;
+      const uint32_t* tb = pb - tj;
+      const int room = na - (int)tj;  // slot tj + d is in A iff d < room
+      load_full_regs<L0, (1 << R)>(ta, tb, room, kx, v);
+    } else {
     const int lane = (int)(tj & 31u);
     const uint32_t wbase = tj & ~31u;  // the warp's part of the slot index
 #pragma unroll
@@ -125,6 +162,7 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
         x = j < na ? __ldg(pa + j) : (j >= N - nbk ? __ldg(pb - j) : ~kx);
       }
       v[e] = x ^ kx;
+    }
     }
   } else {
   {
@@ -184,9 +222,12 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
   Body::template rounds<0>(cx, smem, v, w);
   Body::tail(cx, v, w);
   using LL = typename Body::template L<Body::NRE - 1>;
+  // (A direct 16-byte store from this layout -- lanes 32 bytes apart, half a
+  // sector per instruction -- measured 518 vs 394 us per 2^28-key phase:
+  // L1/LSU-bound.  The shared-memory transpose keeps every store a full
+  // 512-byte warp line.)
   LL::sts(smem, v);
   __syncthreads();
-  uint32_t* o = out + o0;
   if (L == N && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
 #pragma unroll 4
     for (int q = threadIdx.x; q < N / 4; q += T) {
@@ -197,6 +238,59 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
   } else {
     for (int j = threadIdx.x; j < L; j += T) o[j] = smem[smem_pad((uint32_t)j)] ^ kx;
   }
+}
+
+template <int C = kMergeC, int R = 5>
+__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
+merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
+                     uint64_t o_begin, uint64_t o_len, uint32_t kx,
+                     const uint64_t* __restrict__ coranks, uint32_t* __restrict__ out,
+                     uint32_t one, uint32_t mone) {
+  constexpr int N = 1 << C;
+  extern __shared__ uint32_t smem[];
+  const uint64_t c = blockIdx.x;
+  const uint64_t o0 = c * (uint64_t)N;
+  const uint64_t o1 = (o0 + N < o_len) ? o0 + N : o_len;
+  const uint64_t i0 = coranks[c], i1 = coranks[c + 1];
+  merge_tile<C, R>(A, B, i0, i1, o_begin + o1 - i1, (int)(o1 - o0), kx, out + o0, one, mone,
+                   smem);
+}
+
+// ---- merge-path phases (the "mergepath" sort variant) --------------------------
+// Phase p of a sort whose 2^(p-1)-key runs are all ascending (in the order kx
+// selects): the bitonic merger of each run pair, with its p-C large-stride
+// half-cleaner steps replaced by a co-rank partition -- every 2^C-key output
+// tile holds exactly the keys of ranks [t 2^C, (t+1) 2^C) of the pair's merge,
+// which is what the half-cleaners route to it -- and its last C steps run by
+// merge_tile.  One HBM round trip per phase; src -> dst (out of place).
+// Tiles never straddle a pair (2^p >= 2^(C+1)).
+__global__ void mergepath_partition_kernel(const uint32_t* __restrict__ src, int p, uint32_t kx,
+                                           uint64_t* __restrict__ coranks, uint64_t ntiles) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const uint64_t half = uint64_t{1} << (p - 1);
+  const uint64_t o = t << kMergeC;
+  const uint64_t base = o & ~((half << 1) - 1);
+  const uint64_t d = o - base;
+  coranks[t] = d == 0 ? 0 : corank_global(d, src + base, half, src + base + half, half, kx);
+}
+
+template <int C = kMergeC, int R = 5>
+__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
+mergepath_merge_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int p,
+                       uint32_t kx, const uint64_t* __restrict__ coranks, uint32_t one,
+                       uint32_t mone) {
+  constexpr int N = 1 << C;
+  extern __shared__ uint32_t smem[];
+  const uint64_t t = blockIdx.x;
+  const uint64_t half = uint64_t{1} << (p - 1);
+  const uint64_t o = t * (uint64_t)N;
+  const uint64_t base = o & ~((half << 1) - 1);
+  const uint64_t d = o - base;  // the tile's first rank in its pair's merge
+  const uint64_t i0 = coranks[t];
+  const uint64_t i1 = (d + N == (half << 1)) ? half : coranks[t + 1];
+  merge_tile<C, R>(src + base, src + base + half, i0, i1, d + N - i1, N, kx, dst + o, one, mone,
+                   smem);
 }
 
 }  // namespace b200

@@ -111,6 +111,14 @@ b.merge_(dev_t(a), dev_t(c), out)
 torch.cuda.synchronize()
 check("merge 5000+7001", host(out), np.sort(np.concatenate([a, c])))
 
+# merge-path variant: out-of-place tile sort + co-rank partitioned phases
+for k in (15, 18):
+    x = u32(1 << k)
+    t = dev_t(x)
+    b.sort_mergepath_(t)
+    torch.cuda.synchronize()
+    check(f"mergepath 2^{k}", host(t), np.sort(x))
+
 # any length (padded + prefix/merge split)
 x = u32((1 << 16) + 5)
 t = dev_t(x)

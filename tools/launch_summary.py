@@ -26,6 +26,10 @@ def load(path):
 def family(name):
     if "tile_sort" in name:
         return "tile_sort"
+    if "mergepath_merge" in name:
+        return "mergepath_merge"  # the merge-path sort variant's phase tiles
+    if "mergepath_partition" in name:
+        return "mergepath_partition"
     if "merge_bitonic_kernel" in name:
         return "merge_path"  # the merge-path tiles (multi-GPU / host entry)
     if "merge_kernel" in name or "cluster_merge" in name:
