@@ -272,7 +272,14 @@ __global__ void mergepath_partition_kernel(const uint32_t* __restrict__ src, int
   const uint64_t o = t << kMergeC;
   const uint64_t base = o & ~((half << 1) - 1);
   const uint64_t d = o - base;
-  coranks[t] = d == 0 ? 0 : corank_global(d, src + base, half, src + base + half, half, kx);
+  if (d == 0) {
+    coranks[t] = 0;
+    return;
+  }
+  // (a 4-ary search -- three independent probes per level, 14 instead of 27
+  // dependent levels at 2^28 -- measured slower: 19-40 vs 13-33 us per
+  // phase; the extra probe sectors cost more than the saved round trips)
+  coranks[t] = corank_global(d, src + base, half, src + base + half, half, kx);
 }
 
 template <int C = kMergeC, int R = 5>

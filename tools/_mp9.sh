@@ -1,0 +1,31 @@
+mkdir -p gpurun_out/mp9
+cat > /tmp/mp_time.py <<'PY'
+import torch, numpy as np, json, sys, os
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
+import paper_1506_01446_b200 as b
+dev = torch.device("cuda:0")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+for k in (16, 20, 24, 26, 28, 30):
+    n = 1 << k
+    src = torch.from_numpy(b.generate_input(n, 1).view(np.int32)).to(dev).view(torch.uint32)
+    work = src.clone(); ts = []
+    for r in range(8):
+        work.copy_(src); flush.zero_(); torch.cuda._sleep(200000)
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); b.sort_mergepath_(work); e1.record(); torch.cuda.synchronize()
+        if r >= 2: ts.append(e0.elapsed_time(e1))
+    ref = torch.sort(src.view(torch.int32).to(torch.int64) & 0xFFFFFFFF).values
+    ok = torch.equal(work.view(torch.int32).to(torch.int64) & 0xFFFFFFFF, ref); del ref
+    print(json.dumps(dict(k=k, ms=min(ts), med=float(np.median(ts)), ok=ok)), flush=True)
+PY
+cat > /tmp/mp_once.py <<'PY'
+import torch, numpy as np, sys, os
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
+import paper_1506_01446_b200 as b
+n = 1 << 28
+t = torch.from_numpy(b.generate_input(n, 1).view(np.int32)).cuda().view(torch.uint32)
+b.sort_mergepath_(t); torch.cuda.synchronize()
+PY
+python /tmp/mp_time.py > gpurun_out/mp9/time.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "mergepath or jitter" > gpurun_out/mp9/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/mp9/pytest.log
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"tile_sort|mergepath" -c 40 --csv python /tmp/mp_once.py > gpurun_out/mp9/launches.csv 2>&1
