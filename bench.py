@@ -670,7 +670,7 @@ def main():
     # network's fused half-cleaner passes.  Reported beside the headline (which
     # stays the network, the reference's algorithm), same timing discipline.
     variant = None
-    if world == 1 and not batched and args.log2n > 13 and not args.no_variants:
+    if world == 1 and not batched and args.log2n > 14 and not args.no_variants:
         try:
             vt = []
             for i in range(args.warmup + args.steps):
@@ -687,21 +687,18 @@ def main():
             same = bool(np.array_equal(work.view(torch.int32).cpu().numpy().view(np.uint32),
                                        gpu_sorted))
             vms = sum(vt) / len(vt)
-            phases = args.log2n - 13
-            tile_ms = ms * share.get("tile_sort", 0.0) if roofline else 0.0
-            phase_ms = (vms - tile_ms) / phases
+            tile_bits = 14  # the variant's default tile (B200_BITONIC_MERGEPATH_TILE)
             t_roof = pmin(args.log2n) * 8 * n / (hbm * 1e9)
             variant = {
                 "mergepath": {
                     "value": n / (vms * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": vms,
                     "steps": len(vt), "output_equals_network_output": same,
-                    "passes": 1 + phases,
-                    "phase": {"kernels": "mergepath_partition_kernel + mergepath_merge_kernel<13,5>",
-                              "avg_ms": phase_ms, "algorithmic_bytes": 8 * n,
-                              "achieved_gbs": 8 * n / (phase_ms * 1e-3) / 1e9,
-                              "frac": 8 * n / (phase_ms * 1e-3) / 1e9 / hbm,
-                              "method": "(step time - the network's tile-sort time) / phases"},
+                    "passes": 1 + args.log2n - tile_bits,
+                    "kernels": (f"tile_sort_kernel<{tile_bits},5> + per phase "
+                                "mergepath_partition_kernel + mergepath_merge_kernel<13,5>"),
                     "sort_roofline_frac": t_roof / (vms * 1e-3),
+                    "sort_roofline_definition": "the network's P_min(k,15) x 8 B x n / HBM BW, "
+                                                "as for the headline",
                     "api": "b200_bitonic_sort_mergepath_u32 (device pointer, in place, "
                            "n-key scratch from the pool)",
                 }}
