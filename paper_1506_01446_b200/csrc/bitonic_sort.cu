@@ -502,26 +502,25 @@ int merge_window_impl(const uint32_t* A, uint64_t la, const uint32_t* B, uint64_
   b200::merge_partition_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
       A, la, B, lb, o_begin, o_len, key_xor, scratch_coranks, nb);
   constexpr int C = b200::kMergeC;
-  static const int mr = [] {  // keys per thread of the merge tiles (experiment knob)
+  // keys per thread of the merge tiles: 2^6 by default (two shared-memory
+  // trips and coalesced direct stores for full tiles, as the merge-path
+  // phases); B200_BITONIC_MERGE_R=4|5 (experiment knob)
+  static const int mr = [] {
     const char* e = std::getenv("B200_BITONIC_MERGE_R");
-    return e ? std::atoi(e) : 5;
+    return e ? std::atoi(e) : 6;
   }();
   cudaError_t e;
-  if (mr == 4) {
-    const void* fn = reinterpret_cast<const void*>(&b200::merge_bitonic_kernel<C, 4>);
-    e = ensure_attr(fn, C, 1);
-    if (e != cudaSuccess) return cuda_fail(e, "merge kernel attribute");
-    b200::merge_bitonic_kernel<C, 4><<<(unsigned)tiles, b200::threads_for<C, 4>(),
-                                       b200::tile_smem_words(C) * 4, s>>>(
+  auto launch = [&](auto kern, int threads) -> cudaError_t {
+    cudaError_t x = ensure_attr(reinterpret_cast<const void*>(kern), C, 1);
+    if (x != cudaSuccess) return x;
+    kern<<<(unsigned)tiles, threads, b200::tile_smem_words(C) * 4, s>>>(
         A, B, o_begin, o_len, key_xor, scratch_coranks, out, 1u, 0xFFFFFFFFu);
-  } else {
-    const void* fn = reinterpret_cast<const void*>(&b200::merge_bitonic_kernel<C>);
-    e = ensure_attr(fn, C, 1);
-    if (e != cudaSuccess) return cuda_fail(e, "merge kernel attribute");
-    b200::merge_bitonic_kernel<C><<<(unsigned)tiles, b200::threads_for<C, 5>(),
-                                    b200::tile_smem_words(C) * 4, s>>>(
-        A, B, o_begin, o_len, key_xor, scratch_coranks, out, 1u, 0xFFFFFFFFu);
-  }
+    return cudaSuccess;
+  };
+  if (mr == 4) e = launch(&b200::merge_bitonic_kernel<C, 4>, b200::threads_for<C, 4>());
+  else if (mr == 5) e = launch(&b200::merge_bitonic_kernel<C, 5>, b200::threads_for<C, 5>());
+  else e = launch(&b200::merge_bitonic_kernel<C, 6>, b200::threads_for<C, 6>());
+  if (e != cudaSuccess) return cuda_fail(e, "merge kernel attribute");
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "merge launch");
   return B200_OK;
@@ -594,8 +593,17 @@ int mergepath_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xo
     e = launch_pass(q, p, s, 0);
     if (e != cudaSuccess) rc = cuda_fail(e, "merge-path tile sort");
   }
+  // keys per thread of the merge windows: 2^6 (rounds {12..7}, {6..1},
+  // {0}: coalesced stores straight from registers, two shared-memory trips)
+  // measured 7.39 vs 7.72 ms at 2^28 against 2^5 (three trips); knob kept
+  static const int mr = [] {
+    const char* x = std::getenv("B200_BITONIC_MERGEPATH_R");
+    return x ? std::atoi(x) : 6;
+  }();
   if (rc == B200_OK) {
-    e = ensure_attr(reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C>), C, 1);
+    e = ensure_attr(mr == 6 ? reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C, 6>)
+                            : reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C>),
+                    C, 1);
     if (e != cudaSuccess) rc = cuda_fail(e, "merge kernel attribute");
   }
   for (int i = 1; i <= phases && rc == B200_OK; ++i) {
@@ -604,9 +612,15 @@ int mergepath_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xo
     const int p = TC + i;
     b200::mergepath_partition_kernel<<<(unsigned)((wins + 255) / 256), 256, 0, s>>>(
         src, p, kx, cor, wins);
-    b200::mergepath_merge_kernel<C><<<(unsigned)wins, b200::threads_for<C, 5>(),
-                                      b200::tile_smem_words(C) * 4, s>>>(
-        src, dst, p, kx, cor, 1u, 0xFFFFFFFFu);
+    if (mr == 6) {
+      b200::mergepath_merge_kernel<C, 6><<<(unsigned)wins, b200::threads_for<C, 6>(),
+                                           b200::tile_smem_words(C) * 4, s>>>(
+          src, dst, p, kx, cor, 1u, 0xFFFFFFFFu);
+    } else {
+      b200::mergepath_merge_kernel<C><<<(unsigned)wins, b200::threads_for<C, 5>(),
+                                        b200::tile_smem_words(C) * 4, s>>>(
+          src, dst, p, kx, cor, 1u, 0xFFFFFFFFu);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_fail(e, "merge-path phase");
   }

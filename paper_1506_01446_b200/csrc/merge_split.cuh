@@ -222,10 +222,20 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
   Body::template rounds<0>(cx, smem, v, w);
   Body::tail(cx, v, w);
   using LL = typename Body::template L<Body::NRE - 1>;
-  // (A direct 16-byte store from this layout -- lanes 32 bytes apart, half a
-  // sector per instruction -- measured 518 vs 394 us per 2^28-key phase:
-  // L1/LSU-bound.  The shared-memory transpose keeps every store a full
-  // 512-byte warp line.)
+  if constexpr (Body::template direct_ok<LL>()) {
+    // The last round's lanes own consecutive vectors (64 keys per thread:
+    // rounds {12..7}, {6..1}, {0}+fillers): coalesced stores straight from
+    // registers, one shared-memory round trip fewer than the transpose below.
+    if (L == N && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+      cx.gout = kx;
+      Body::store(cx, smem, v, w);
+      return;
+    }
+  }
+  // (A direct 16-byte store from a layout whose lanes sit 32 bytes apart --
+  // half a sector per instruction -- measured 518 vs 394 us per 2^28-key
+  // phase: L1/LSU-bound.  The shared-memory transpose keeps every store a
+  // full 512-byte warp line.)
   LL::sts(smem, v);
   __syncthreads();
   if (L == N && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
@@ -282,8 +292,13 @@ __global__ void mergepath_partition_kernel(const uint32_t* __restrict__ src, int
   coranks[t] = corank_global(d, src + base, half, src + base + half, half, kx);
 }
 
+// (capping the 64-key variant at 80 registers for six CTAs per SM measured
+// slower than 86 registers and five: 2^28 8.00 vs 7.39 ms)
+#ifndef B200_MP_MINB6
+#define B200_MP_MINB6 4
+#endif
 template <int C = kMergeC, int R = 5>
-__global__ void __launch_bounds__(threads_for<C, R>(), min_blocks_for<C, R>())
+__global__ void __launch_bounds__(threads_for<C, R>(), R == 6 ? B200_MP_MINB6 : min_blocks_for<C, R>())
 mergepath_merge_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int p,
                        uint32_t kx, const uint64_t* __restrict__ coranks, uint32_t one,
                        uint32_t mone) {
