@@ -570,10 +570,14 @@ int mergepath_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xo
   int rc = B200_OK;
   // phase i (1-based) writes buf[i & 1]; the tile sort writes buf[0]
   uint32_t* buf[2] = {(phases & 1) ? tmp : d_keys, (phases & 1) ? d_keys : tmp};
+  static const int tile_r = [] {  // keys per thread of the tile sort (experiment knob)
+    const char* x = std::getenv("B200_BITONIC_MERGEPATH_TILE_R");
+    return x ? std::atoi(x) : 5;
+  }();
   {
     b200::PlanPass q;
     q.C = TC;
-    q.R = 5;
+    q.R = tile_r;
     q.a = q.y = TC;
     q.tile_sort = 1;
     q.p_end = TC;
