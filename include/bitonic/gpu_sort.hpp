@@ -80,6 +80,16 @@ inline void sort_device(std::uint32_t* d_keys, std::uint64_t n, bool ascending =
                         b200_stream_t stream = nullptr) {
   check(b200_bitonic_sort_u32(d_keys, n, ascending ? 0 : 1, stream));
 }
+// The merge-path variant: same output, one HBM pass per global phase
+// (allocates an n-key scratch buffer from the library's pool).
+inline void sort_device_mergepath(std::int32_t* d_keys, std::uint64_t n, bool ascending = true,
+                                  b200_stream_t stream = nullptr) {
+  check(b200_bitonic_sort_mergepath_i32(d_keys, n, ascending ? 0 : 1, stream));
+}
+inline void sort_device_mergepath(std::uint32_t* d_keys, std::uint64_t n, bool ascending = true,
+                                  b200_stream_t stream = nullptr) {
+  check(b200_bitonic_sort_mergepath_u32(d_keys, n, ascending ? 0 : 1, stream));
+}
 inline void sort_device_batched(std::uint32_t* d_keys, std::uint64_t n_per_array,
                                 std::uint64_t batch, bool ascending = true,
                                 b200_stream_t stream = nullptr) {
