@@ -695,7 +695,7 @@ def main():
                     "steps": len(vt), "output_equals_network_output": same,
                     "passes": 1 + args.log2n - tile_bits,
                     "kernels": (f"tile_sort_kernel<{tile_bits},5> + per phase "
-                                "mergepath_partition_kernel + mergepath_merge_kernel<13,5>"),
+                                "mergepath_partition_kernel + mergepath_merge_kernel<13,6>"),
                     "sort_roofline_frac": t_roof / (vms * 1e-3),
                     "sort_roofline_definition": "the network's P_min(k,15) x 8 B x n / HBM BW, "
                                                 "as for the headline",
