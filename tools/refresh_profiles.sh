@@ -8,7 +8,7 @@ out=gpurun_out/prof
 mkdir -p $out
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 for cfg in "28" "24" "20" "16"; do
-  cmd="python bench.py --log2n $cfg --steps 2 --warmup 3 --no-cpu-baseline"
+  cmd="python bench.py --log2n $cfg --steps 2 --warmup 3 --no-cpu-baseline --no-variants"
   if $cmd > $out/bench_k$cfg.json 2> $out/bench_k$cfg.err; then
     ncu --metrics $M --clock-control none --csv --log-file $out/launches_k$cfg.csv $cmd > /dev/null 2>&1
   fi
