@@ -557,6 +557,7 @@ int mergepath_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xo
     return fail(B200_CONFIG, "device pointers must be 16-byte aligned");
   }
   const uint32_t kx = key_xor ^ (descending ? 0xFFFFFFFFu : 0u);
+  uint32_t kx_arg = kx;
   const int phases = k - TC;
   const uint64_t wins = n >> C;
   uint32_t* tmp = nullptr;
@@ -610,22 +611,42 @@ int mergepath_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xo
                     C, 1);
     if (e != cudaSuccess) rc = cuda_fail(e, "merge kernel attribute");
   }
+  // every phase kernel is launched with programmatic dependent launch: its
+  // CTAs become resident while the previous kernel drains and wait in
+  // griddepcontrol.wait for its memory (the kernels call pdl_wait first)
+  auto pdl_launch = [&](const void* fn, unsigned grid, unsigned block, size_t smem,
+                        void** args) -> cudaError_t {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl.load() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+  };
+  const void* merge_fn = mr == 6
+                             ? reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C, 6>)
+                             : reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C>);
+  const unsigned merge_threads =
+      mr == 6 ? b200::threads_for<C, 6>() : b200::threads_for<C, 5>();
   for (int i = 1; i <= phases && rc == B200_OK; ++i) {
     const uint32_t* src = buf[(i - 1) & 1];
     uint32_t* dst = buf[i & 1];
-    const int p = TC + i;
-    b200::mergepath_partition_kernel<<<(unsigned)((wins + 255) / 256), 256, 0, s>>>(
-        src, p, kx, cor, wins);
-    if (mr == 6) {
-      b200::mergepath_merge_kernel<C, 6><<<(unsigned)wins, b200::threads_for<C, 6>(),
-                                           b200::tile_smem_words(C) * 4, s>>>(
-          src, dst, p, kx, cor, 1u, 0xFFFFFFFFu);
-    } else {
-      b200::mergepath_merge_kernel<C><<<(unsigned)wins, b200::threads_for<C, 5>(),
-                                        b200::tile_smem_words(C) * 4, s>>>(
-          src, dst, p, kx, cor, 1u, 0xFFFFFFFFu);
+    int p = TC + i;
+    uint32_t one = 1u, mone = 0xFFFFFFFFu;
+    uint64_t nw = wins;
+    void* pargs[] = {&src, &p, &kx_arg, &cor, &nw};
+    e = pdl_launch(reinterpret_cast<const void*>(&b200::mergepath_partition_kernel),
+                   (unsigned)((wins + 255) / 256), 256, 0, pargs);
+    if (e == cudaSuccess) {
+      void* margs[] = {&src, &dst, &p, &kx_arg, &cor, &one, &mone};
+      e = pdl_launch(merge_fn, (unsigned)wins, merge_threads,
+                     (size_t)b200::tile_smem_words(C) * 4, margs);
     }
-    e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_fail(e, "merge-path phase");
   }
   cudaFreeAsync(cor, s);

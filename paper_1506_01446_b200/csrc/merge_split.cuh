@@ -277,6 +277,8 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
 __global__ void mergepath_partition_kernel(const uint32_t* __restrict__ src, int p, uint32_t kx,
                                            uint64_t* __restrict__ coranks, uint64_t ntiles) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();  // the previous phase's output (PDL launch; no-op otherwise)
+  pdl_trigger();
   if (t >= ntiles) return;
   const uint64_t half = uint64_t{1} << (p - 1);
   const uint64_t o = t << kMergeC;
@@ -309,10 +311,12 @@ mergepath_merge_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ 
   const uint64_t o = t * (uint64_t)N;
   const uint64_t base = o & ~((half << 1) - 1);
   const uint64_t d = o - base;  // the tile's first rank in its pair's merge
+  pdl_wait();  // the partition's coranks (PDL launch; no-op otherwise)
   const uint64_t i0 = coranks[t];
   const uint64_t i1 = (d + N == (half << 1)) ? half : coranks[t + 1];
   merge_tile<C, R>(src + base, src + base + half, i0, i1, d + N - i1, N, kx, dst + o, one, mone,
                    smem);
+  pdl_trigger();
 }
 
 }  // namespace b200
