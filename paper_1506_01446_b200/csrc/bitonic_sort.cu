@@ -628,24 +628,39 @@ int mergepath_impl(uint32_t* d_keys, uint64_t n, int descending, uint32_t key_xo
     cfg.numAttrs = 1;
     return cudaLaunchKernelExC(&cfg, fn, args);
   };
-  const void* merge_fn = mr == 6
-                             ? reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C, 6>)
-                             : reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C>);
-  const unsigned merge_threads =
-      mr == 6 ? b200::threads_for<C, 6>() : b200::threads_for<C, 5>();
+  // merge-window size: 2^13 keys (experiment knob B200_BITONIC_MERGEPATH_WIN=14)
+  static const int wb_env = [] {
+    const char* x = std::getenv("B200_BITONIC_MERGEPATH_WIN");
+    return x ? std::atoi(x) : 13;
+  }();
+  const int WB = (wb_env == 14 && TC >= 14) ? 14 : 13;
+  const uint64_t nwin = n >> WB;
+  const void* merge_fn =
+      WB == 14 ? reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<14, 6>)
+      : mr == 6 ? reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C, 6>)
+                : reinterpret_cast<const void*>(&b200::mergepath_merge_kernel<C>);
+  const void* part_fn = WB == 14
+                            ? reinterpret_cast<const void*>(&b200::mergepath_partition_kernel<14>)
+                            : reinterpret_cast<const void*>(&b200::mergepath_partition_kernel<C>);
+  const unsigned merge_threads = WB == 14   ? b200::threads_for<14, 6>()
+                                 : mr == 6 ? b200::threads_for<C, 6>()
+                                           : b200::threads_for<C, 5>();
+  if (WB == 14 && rc == B200_OK) {
+    e = ensure_attr(merge_fn, 14, 1);
+    if (e != cudaSuccess) rc = cuda_fail(e, "merge kernel attribute");
+  }
   for (int i = 1; i <= phases && rc == B200_OK; ++i) {
     const uint32_t* src = buf[(i - 1) & 1];
     uint32_t* dst = buf[i & 1];
     int p = TC + i;
     uint32_t one = 1u, mone = 0xFFFFFFFFu;
-    uint64_t nw = wins;
+    uint64_t nw = nwin;
     void* pargs[] = {&src, &p, &kx_arg, &cor, &nw};
-    e = pdl_launch(reinterpret_cast<const void*>(&b200::mergepath_partition_kernel),
-                   (unsigned)((wins + 255) / 256), 256, 0, pargs);
+    e = pdl_launch(part_fn, (unsigned)((nwin + 255) / 256), 256, 0, pargs);
     if (e == cudaSuccess) {
       void* margs[] = {&src, &dst, &p, &kx_arg, &cor, &one, &mone};
-      e = pdl_launch(merge_fn, (unsigned)wins, merge_threads,
-                     (size_t)b200::tile_smem_words(C) * 4, margs);
+      e = pdl_launch(merge_fn, (unsigned)nwin, merge_threads,
+                     (size_t)b200::tile_smem_words(WB) * 4, margs);
     }
     if (e != cudaSuccess) rc = cuda_fail(e, "merge-path phase");
   }

@@ -274,6 +274,7 @@ merge_bitonic_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict_
 // which is what the half-cleaners route to it -- and its last C steps run by
 // merge_tile.  One HBM round trip per phase; src -> dst (out of place).
 // Tiles never straddle a pair (2^p >= 2^(C+1)).
+template <int WB = kMergeC>
 __global__ void mergepath_partition_kernel(const uint32_t* __restrict__ src, int p, uint32_t kx,
                                            uint64_t* __restrict__ coranks, uint64_t ntiles) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -281,7 +282,7 @@ __global__ void mergepath_partition_kernel(const uint32_t* __restrict__ src, int
   pdl_trigger();
   if (t >= ntiles) return;
   const uint64_t half = uint64_t{1} << (p - 1);
-  const uint64_t o = t << kMergeC;
+  const uint64_t o = t << WB;
   const uint64_t base = o & ~((half << 1) - 1);
   const uint64_t d = o - base;
   if (d == 0) {
@@ -300,7 +301,7 @@ __global__ void mergepath_partition_kernel(const uint32_t* __restrict__ src, int
 #define B200_MP_MINB6 4
 #endif
 template <int C = kMergeC, int R = 5>
-__global__ void __launch_bounds__(threads_for<C, R>(), R == 6 ? B200_MP_MINB6 : min_blocks_for<C, R>())
+__global__ void __launch_bounds__(threads_for<C, R>(), (R == 6 && C == 13) ? B200_MP_MINB6 : min_blocks_for<C, R>())
 mergepath_merge_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int p,
                        uint32_t kx, const uint64_t* __restrict__ coranks, uint32_t one,
                        uint32_t mone) {
