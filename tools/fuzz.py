@@ -20,12 +20,13 @@ def tot64(u):
 
 
 while time.time() - t0 < budget:
-    kind = rng.choice(["sort", "padded", "batched", "pairs", "f32", "i64", "f64", "planes"])
+    kind = rng.choice(["sort", "mergepath", "padded", "batched", "pairs", "f32", "i64", "f64",
+                       "planes"])
     desc = bool(rng.integers(0, 2))
     k = int(rng.integers(1, kmax + 1))
     n = 1 << k
     try:
-        if kind in ("sort", "padded", "batched", "pairs"):
+        if kind in ("sort", "mergepath", "padded", "batched", "pairs"):
             dt = np.int32 if rng.integers(0, 2) else np.uint32
             if kind == "padded":
                 n = int(rng.integers(1, 1 << 23))
@@ -37,6 +38,8 @@ while time.time() - t0 < budget:
             tv = t.view(torch.uint32) if dt == np.uint32 else t
             if kind == "sort":
                 b.sort_(tv, descending=desc); want = np.sort(x)
+            elif kind == "mergepath":
+                b.sort_mergepath_(tv, descending=desc); want = np.sort(x)
             elif kind == "padded":
                 b.sort_padded_(tv, descending=desc); want = np.sort(x)
             elif kind == "batched":
